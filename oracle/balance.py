@@ -1,0 +1,156 @@
+"""Padding-exchange load balancer (§IV-B-1, Fig. fig-exchange-padding).
+ORACLE: test infrastructure only.  Plain Python.
+
+The paper's three steps, on the valid-token counts the all-gather makes
+identical on every worker:
+  1. all-gather: global sample id g = r*B + k (rank-major concatenation).
+  2. "Sort the all-gathered input sequences ... according to the valid token number"
+     (P:357); ties broken by global id ascending (reading R11).
+  3. "Interleave slicing": worker i takes sorted positions i, i+W, i+2W, ...,
+     in that order (reading R12).
+
+Also here (reading R15): the snake (boustrophedon) deal, and a brute-force search
+for the min-max-tokens partition with equal cardinality B, by two independent
+enumerators, with the canonical tie-break "lexicographically smallest perm vector".
+
+Outputs use the library's layout: perm[r*B + k] = global id of the k-th sample on
+rank r; rank_tokens[r]; send_samples[src*W + dst]; send_tokens[src*W + dst].
+
+Pins (tests/test_oracle_balance.py): SPEC worked examples (S:316 tie order, S:326 W=2
+positions 0,2,4, S:336 [[512,512],[64,64]] -> 576/576), permutation + cardinality,
+spread <= Lmax - Lmin, brute force agreement of the two enumerators, the
+counterexample [1,2,3,4] (paper 4/6 vs optimum 5/5), W=1 and B=1 special cases.
+Parity pinned.
+"""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+
+
+def _check(all_lengths, W, B):
+    a = [int(x) for x in all_lengths]
+    if W < 1 or B < 1 or len(a) != W * B:
+        raise ValueError("shape: need W*B lengths")
+    if any(x < 1 for x in a):
+        raise ValueError("length must be >= 1")
+    return a
+
+
+def sort_by_valid_tokens(all_lengths):
+    """Global ids ordered by (valid tokens asc, id asc) -- P:357 + R11."""
+    a = list(all_lengths)
+    return sorted(range(len(a)), key=lambda g: (a[g], g))
+
+
+def plan_from_groups(all_lengths, W, B, groups):
+    """perm / rank_tokens / send matrices for a list of W per-rank id lists."""
+    a = list(all_lengths)
+    perm = np.zeros(W * B, dtype=np.int64)
+    rank_tokens = np.zeros(W, dtype=np.int64)
+    send_samples = np.zeros(W * W, dtype=np.int64)
+    send_tokens = np.zeros(W * W, dtype=np.int64)
+    for dst in range(W):
+        assert len(groups[dst]) == B
+        for k, g in enumerate(groups[dst]):
+            perm[dst * B + k] = g
+            rank_tokens[dst] += a[g]
+            src = g // B
+            send_samples[src * W + dst] += 1
+            send_tokens[src * W + dst] += a[g]
+    return {"perm": perm, "rank_tokens": rank_tokens,
+            "send_samples": send_samples, "send_tokens": send_tokens}
+
+
+def balance_paper(all_lengths, W, B):
+    """NVIDIA/paper padding exchange: sort + interleave slice."""
+    a = _check(all_lengths, W, B)
+    order = sort_by_valid_tokens(a)
+    groups = [[order[i + k * W] for k in range(B)] for i in range(W)]
+    return plan_from_groups(a, W, B, groups)
+
+
+def balance_snake(all_lengths, W, B):
+    """Snake deal of the same sorted list: round r goes to ranks 0..W-1 when r is even
+    and W-1..0 when r is odd (a variant of P:359, reading R15(iv))."""
+    a = _check(all_lengths, W, B)
+    order = sort_by_valid_tokens(a)
+    groups = [[] for _ in range(W)]
+    for r in range(B):
+        for s in range(W):
+            dst = s if r % 2 == 0 else W - 1 - s
+            groups[dst].append(order[r * W + s])
+    return plan_from_groups(a, W, B, groups)
+
+
+def _canon_group(a, grp):
+    return tuple(sorted(grp, key=lambda g: (a[g], g)))
+
+
+def partitions_recursive(n, W, B):
+    """Enumerator 1: unlabeled partitions of range(n) into W groups of B, by taking the
+    smallest remaining id and choosing its B-1 companions."""
+    def rec(rem):
+        if not rem:
+            yield []
+            return
+        first, rest = rem[0], rem[1:]
+        for comp in itertools.combinations(rest, B - 1):
+            left = [x for x in rest if x not in comp]
+            for tail in rec(left):
+                yield [(first,) + comp] + tail
+    yield from rec(list(range(n)))
+
+
+def partitions_labelings(n, W, B):
+    """Enumerator 2: all W**n labelings, keep those with exactly B per label, dedupe to
+    unlabeled partitions.  Only for tiny W**n."""
+    seen = set()
+    for lab in itertools.product(range(W), repeat=n):
+        counts = [0] * W
+        for x in lab:
+            counts[x] += 1
+        if any(c != B for c in counts):
+            continue
+        groups = [tuple(i for i in range(n) if lab[i] == r) for r in range(W)]
+        key = tuple(sorted(groups))
+        if key not in seen:
+            seen.add(key)
+            yield [list(g) for g in key]
+
+
+def balance_opt(all_lengths, W, B, enumerator="recursive"):
+    """Brute-force optimum: minimise the max per-rank token count over all equal-
+    cardinality partitions; among optima return the lexicographically smallest perm
+    vector (groups laid out in (length, id) order inside a rank)."""
+    a = _check(all_lengths, W, B)
+    n = W * B
+    gen = partitions_recursive(n, W, B) if enumerator == "recursive" else partitions_labelings(n, W, B)
+    best_val, best_perm, best_groups = None, None, None
+    for part in gen:
+        val = max(sum(a[g] for g in grp) for grp in part)
+        if best_val is not None and val > best_val:
+            continue
+        groups = sorted(_canon_group(a, grp) for grp in part)   # lexicographic labelling
+        perm = [g for grp in groups for g in grp]
+        if best_val is None or val < best_val or perm < best_perm:
+            best_val, best_perm, best_groups = val, perm, groups
+    out = plan_from_groups(a, W, B, [list(g) for g in best_groups])
+    out["opt_max_tokens"] = best_val
+    return out
+
+
+def cu_seqlens_for_rank(all_lengths, perm, W, B, rank):
+    """batch_offset of rank's post-exchange batch (P:302 on the rebalanced samples)."""
+    a = list(all_lengths)
+    out = [0]
+    for k in range(B):
+        out.append(out[-1] + a[int(perm[rank * B + k])])
+    return np.asarray(out, dtype=np.int64)
+
+
+def imbalance(rank_tokens) -> float:
+    """max_r / mean_r - 1 (reading R14; S:296 defines max/mean)."""
+    t = np.asarray(rank_tokens, dtype=np.float64)
+    return float(t.max() / t.mean() - 1.0)

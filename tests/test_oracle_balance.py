@@ -1,0 +1,132 @@
+"""Pins for oracle.balance and oracle.exchange -- CPU only."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import balance, exchange, varlen
+import synth
+
+
+def test_spec_worked_examples(golden):
+    g = golden["spec_worked_examples"]
+    ex = g["sort_by_valid_tokens"][0]
+    assert balance.sort_by_valid_tokens(ex["counts"]) == ex["order"], ex["cite"]
+    ex = g["interleave_slice"][0]
+    lens = list(range(1, ex["n"] + 1))                 # already sorted: position == id
+    plan = balance.balance_paper(lens, ex["W"], ex["n"] // ex["W"])
+    B = ex["n"] // ex["W"]
+    assert plan["perm"][ex["worker"] * B:(ex["worker"] + 1) * B].tolist() == ex["positions"]
+    ex = g["exchange_padding"][0]
+    flat = [x for r in ex["lengths"] for x in r]
+    plan = balance.balance_paper(flat, ex["W"], ex["B"])
+    assert plan["rank_tokens"].tolist() == ex["rank_tokens"], ex["cite"]
+
+
+def _invariants(plan, a, W, B):
+    perm = plan["perm"]
+    assert sorted(perm.tolist()) == list(range(W * B))                  # permutation
+    for r in range(W):
+        grp = perm[r * B:(r + 1) * B]
+        assert len(grp) == B                                            # cardinality
+        assert plan["rank_tokens"][r] == sum(a[g] for g in grp)
+    ss = plan["send_samples"].reshape(W, W)
+    assert np.all(ss.sum(axis=1) == B) and np.all(ss.sum(axis=0) == B)
+    st = plan["send_tokens"].reshape(W, W)
+    assert np.array_equal(st.sum(axis=0), plan["rank_tokens"])
+
+
+def test_paper_mode_invariants_and_spread_bound():
+    for W, B, seed in [(2, 56, 0), (4, 56, 1), (8, 56, 2), (3, 5, 3), (8, 1, 4), (1, 9, 5)]:
+        a = synth.gen_lengths("mlperf_like_v0", W * B, seed).tolist()
+        plan = balance.balance_paper(a, W, B)
+        _invariants(plan, a, W, B)
+        t = plan["rank_tokens"]
+        assert t.max() - t.min() <= max(a) - min(a)                     # S:353 telescoping bound
+        # interleave order inside a rank is ascending length (R12)
+        for r in range(W):
+            lens = [a[g] for g in plan["perm"][r * B:(r + 1) * B]]
+            assert lens == sorted(lens)
+        # determinism
+        assert np.array_equal(balance.balance_paper(a, W, B)["perm"], plan["perm"])
+
+
+def test_paper_mode_imbalance_gate_at_8():
+    """BASELINE gate: max-over-ranks imbalance <= 5% at 8 GPUs, B=56 (proof bound 3.2%)."""
+    for step in range(20):
+        a = synth.skewed_rank_lengths(8, 56, step, "sorted-block").reshape(-1)
+        plan = balance.balance_paper(a, 8, 56)
+        assert balance.imbalance(plan["rank_tokens"]) <= 0.05
+
+
+def test_two_enumerators_agree():
+    rng = np.random.default_rng(0)
+    for W, B in [(2, 2), (2, 3), (3, 2), (2, 4), (3, 3), (2, 5), (4, 2)]:
+        n = W * B
+        if W ** n > 300000:
+            continue
+        for _ in range(3):
+            a = rng.integers(1, 20, size=n).tolist()
+            r1 = balance.balance_opt(a, W, B, "recursive")
+            r2 = balance.balance_opt(a, W, B, "labelings")
+            assert r1["opt_max_tokens"] == r2["opt_max_tokens"]
+            assert np.array_equal(r1["perm"], r2["perm"])
+
+
+def test_opt_is_optimal_by_plain_search():
+    """Independent check of the optimum: plain search over all permutations of the ids."""
+    rng = np.random.default_rng(1)
+    for W, B in [(2, 2), (2, 3), (3, 2)]:
+        a = rng.integers(1, 50, size=W * B).tolist()
+        best = min(max(sum(a[g] for g in perm[r * B:(r + 1) * B]) for r in range(W))
+                   for perm in itertools.permutations(range(W * B)))
+        assert balance.balance_opt(a, W, B)["opt_max_tokens"] == best
+
+
+def test_counterexample_and_bounds_vs_opt():
+    plan = balance.balance_paper([1, 2, 3, 4], 2, 2)
+    assert sorted(plan["rank_tokens"].tolist()) == [4, 6]               # the paper's rule
+    assert balance.balance_opt([1, 2, 3, 4], 2, 2)["opt_max_tokens"] == 5   # the optimum
+    rng = np.random.default_rng(2)
+    for _ in range(60):
+        W, B = [(2, 2), (2, 3), (3, 2), (2, 4), (3, 3), (4, 2), (2, 5)][rng.integers(0, 7)]
+        a = rng.integers(1, 513, size=W * B).tolist()
+        opt = balance.balance_opt(a, W, B)["opt_max_tokens"]
+        pm = balance.balance_paper(a, W, B)["rank_tokens"].max()
+        sn = balance.balance_snake(a, W, B)["rank_tokens"].max()
+        assert opt <= sn <= pm                                          # snake never worse than paper
+        assert pm - opt <= (W - 1) / W * (max(a) - min(a)) + 1e-9
+        if B <= 2:
+            assert sn == opt                                            # snake optimal for B <= 2
+
+
+def test_special_cases():
+    a = [9, 3, 5]
+    assert balance.balance_paper(a, 1, 3)["perm"].tolist() == [1, 2, 0]   # W=1: sorted order
+    assert balance.balance_opt(a, 1, 3)["opt_max_tokens"] == 17
+    p = balance.balance_paper([4, 1, 3], 3, 1)                            # B=1: one per rank
+    assert p["perm"].tolist() == [1, 2, 0]
+    with pytest.raises(ValueError):
+        balance.balance_paper([1, 2, 3], 2, 2)                            # W*B not full (R13)
+    with pytest.raises(ValueError):
+        balance.balance_paper([1, 0], 2, 1)
+
+
+def test_exchange_simulation():
+    W, B, rec, srec = 3, 4, 16, 4
+    lens = synth.gen_lengths("uniform", W * B, 11, max_seqlen=32).reshape(W, B)
+    toks = [synth.gen_bytes(int(lens[r].sum()) * rec, 20 + r).reshape(-1, rec) for r in range(W)]
+    smps = [synth.gen_bytes(B * srec, 30 + r).reshape(B, srec) for r in range(W)]
+    plan = balance.balance_paper(lens.reshape(-1), W, B)
+    out = exchange.exchange(lens, toks, smps, plan["perm"], W, B)
+    offs = [varlen.batch_offset(lens[r]) for r in range(W)]
+    all_rows = sorted(bytes(x) for r in range(W) for x in toks[r])
+    got_rows = sorted(bytes(x) for d in range(W) for x in out[d]["tokens"])
+    assert all_rows == got_rows                                            # multiset preserved
+    for d in range(W):
+        assert out[d]["cu"][-1] == plan["rank_tokens"][d]
+        for k in range(B):
+            g = int(plan["perm"][d * B + k]); s, kk = divmod(g, B)
+            a0, a1 = out[d]["cu"][k], out[d]["cu"][k + 1]
+            assert np.array_equal(out[d]["tokens"][a0:a1], toks[s][offs[s][kk]:offs[s][kk + 1]])
+            assert np.array_equal(out[d]["samples"][k], smps[s][kk])
