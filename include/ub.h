@@ -1,0 +1,224 @@
+/*
+ * ub.h -- C ABI of the unpadded-BERT data-parallel hot path for NVIDIA B200 (sm_100a).
+ *
+ * Paper: "Boosting Distributed Training Performance of the Unpadded BERT Model",
+ * arXiv 2208.08124.  Citations "P:<n>" are lines of the paper text;
+ * readings "R<k>" are listed in DESIGN.md §2.
+ *
+ * Conventions (all entry points):
+ *   - Plain C types only.  Device pointers are CUDA device addresses; "h_" pointers are
+ *     host memory.  `stream` is a cudaStream_t handle passed as void* (NULL = legacy
+ *     default stream).
+ *   - Ownership: the caller allocates and frees every buffer and keeps it alive until
+ *     the work enqueued on `stream` has completed.  The library never allocates caller
+ *     memory; the only library-owned object is `ub_comm`.
+ *   - Asynchrony: device entry points only enqueue work on `stream` and never
+ *     synchronise the host (the method exists to avoid host<->device syncs).
+ *     The one exception is ub_balance_exchange (documented there).
+ *   - Errors: arguments are validated on the host before anything is launched; on a
+ *     non-OK status nothing was enqueued and ub_last_error() returns a thread-local
+ *     message.  Device-resident data (cu_seqlens monotonicity, lengths <= max_seqlen)
+ *     is NOT validated on the fast path: that would need a sync.
+ *   - Packed ("unpadded") layout (Fig. fig-storage): the batch and sequence
+ *     dimensions are merged and only valid tokens are stored; cu_seqlens (the paper's
+ *     batch_offset) is the int32 prefix sum [B+1] with cu[0] = 0, cu[B] = T.
+ */
+#ifndef UB_H_
+#define UB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  UB_OK = 0,
+  UB_ERR_INVALID_ARG = 1,  /* null pointer, bad enum, empty batch, length < 1, scale <= 0, p outside [0,1) */
+  UB_ERR_INVALID_MASK = 2, /* non-prefix input_mask row */
+  UB_ERR_CAPACITY = 3,     /* a length exceeds max_seqlen / padded capacity */
+  UB_ERR_SHAPE = 4,        /* inconsistent sizes (W*B lengths, row_bytes <= 0, T mismatch) */
+  UB_ERR_UNSUPPORTED = 5,  /* dtype / head_dim / device (needs sm_100) / mode limits */
+  UB_ERR_CUDA = 6,         /* a CUDA runtime call failed */
+  UB_ERR_NCCL = 7          /* an NCCL call failed */
+} ub_status;
+
+typedef enum { UB_BF16 = 0, UB_FP32 = 1 } ub_dtype;
+
+/* Thread-local message describing the last non-OK status of this thread ("" if none). */
+const char* ub_last_error(void);
+/* Library build string (arch, version). */
+const char* ub_version(void);
+
+/* ------------------------------------------------------------------------------------
+ * batch_offset / cu_seqlens ("a prefix sum array ... to record the token number
+ * of each sequence").  Host helper.
+ *   h_lengths [B] int32, each 1 <= L <= max_seqlen (else UB_ERR_INVALID_ARG / _CAPACITY);
+ *   h_cu [B+1] int32 output, exclusive prefix sum with trailing total.
+ *   The total must fit in int32 (else UB_ERR_SHAPE).
+ */
+ub_status ub_cu_seqlens(const int32_t* h_lengths, int32_t B, int32_t max_seqlen, int32_t* h_cu);
+
+/* Lengths from a padded input_mask [B, S] int32 (0/1) on the host ("The valid input
+ * token number can be obtained from the input tensor input_mask").  A row that is not a
+ * prefix of ones followed by zeros -> UB_ERR_INVALID_MASK. */
+ub_status ub_lengths_from_mask(const int32_t* h_mask, int32_t B, int32_t S, int32_t* h_lengths);
+
+/* ------------------------------------------------------------------------------------
+ * Unpad = gather ("input data are compressed to the unpad format ... obtained by
+ * the gather operator").  padded [B, S, row_bytes] -> packed [T, row_bytes]:
+ *   packed[cu[b] + i] = padded[b][i]  for i < cu[b+1]-cu[b].
+ * Rows are opaque row_bytes-wide records (int32 ids, bf16 hidden rows, ...).
+ * d_cu: device [B+1].  T must equal cu[B] (not checked: device-resident).
+ * 16-B vector path when row_bytes % 16 == 0 and both pointers are 16-B aligned,
+ * else a 4-B or 1-B path (not an error).
+ */
+ub_status ub_unpad(const void* padded, void* packed, const int32_t* d_cu, int32_t B, int32_t S,
+                   int64_t T, int64_t row_bytes, void* stream);
+
+/* Pad = scatter ("uncompressed to the padding format by using a scatter operator").
+ * packed [T, row_bytes] -> padded [B, S, row_bytes]; positions i >= L_b receive the
+ * row_bytes pattern at d_pad_row (device), or zeros when d_pad_row is NULL. */
+ub_status ub_pad(const void* packed, void* padded, const int32_t* d_cu, int32_t B, int32_t S,
+                 int64_t T, int64_t row_bytes, const void* d_pad_row, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Varlen fused multi-head attention, Eq. (1):
+ *     O = softmax(scale * Q K^T) V   per sequence b and head h, within the sequence only
+ * (unpadded FMHA over packed tokens; no cross-sequence attention, R2), with
+ * optional inverted dropout on the probabilities (R4) from the counter-based Philox
+ * mask of R5 keyed by (seed, offset).
+ *
+ * Work is grouped by length: a device-side plan buckets sequences by their number of
+ * 128-token tiles -- the paper's groups (0,128] (128,256] (256,384] (384,512]
+ * -- and one persistent launch processes the buckets longest-first, in place of the
+ * paper's one-kernel-per-group multi-stream launch.
+ *
+ * Layouts: qkv [T, 3, H, D] (the QKV GEMM output [T, 3*H*D]); out, dout [T, H, D];
+ * lse [H, T] fp32 natural log (LSE_t = max + log sum exp, before dropout);
+ * dqkv [T, 3, H, D].  dtype UB_BF16 (tcgen05 tensor-core path, D == 64) or UB_FP32
+ * (exact-fp32 CUDA-core path, D <= 128, for tiny checks).
+ * ws: device workspace of ub_fmha_workspace_bytes() bytes, 256-B aligned, owned by the
+ * caller; contents need no initialisation and are scratch between calls (one call at a
+ * time per workspace).
+ */
+typedef struct {
+  int32_t B;          /* number of sequences (>= 1) */
+  int64_t T;          /* total valid tokens = cu[B] (>= 1) */
+  int32_t max_seqlen; /* >= every length; bounds the per-sequence tile count */
+  int32_t heads;      /* H >= 1 */
+  int32_t head_dim;   /* D: 64 for UB_BF16; 1..128 for UB_FP32 */
+  float scale;        /* > 0; 1/sqrt(D) in BERT (R1) */
+  float p_dropout;    /* in [0, 1); 0 disables the RNG entirely */
+  uint64_t seed;      /* Philox key (R5) */
+  uint64_t offset;    /* Philox counter word 3 (low 32 bits used) */
+  int32_t dtype;      /* ub_dtype */
+} ub_fmha_params;
+
+size_t ub_fmha_workspace_bytes(const ub_fmha_params* prm, int is_bwd);
+
+ub_status ub_varlen_fmha_fwd(const ub_fmha_params* prm, const void* qkv, const int32_t* d_cu,
+                             void* out, float* lse, void* ws, void* stream);
+
+/* Backward: given dO, returns dQ, dK, dV (R4/R5 dropout replayed from the same key):
+ *   Delta_i = sum_d dO_id O_id;  dV = P~^T dO;  dP = (dO V^T) * M/(1-p);
+ *   dS = P * (dP - Delta);  dQ = scale dS K;  dK = scale dS^T Q. */
+ub_status ub_varlen_fmha_bwd(const ub_fmha_params* prm, const void* qkv, const void* out,
+                             const float* lse, const void* dout, const int32_t* d_cu,
+                             void* dqkv, void* ws, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Padding-exchange balancer (§IV-B-1).  Pure host function: deterministic,
+ * byte-identical on every rank given the same all-gathered lengths.
+ *   h_all_lengths [W*B]: rank-major all-gather of the valid lengths, global id g = r*B+k.
+ *   UB_BAL_PAPER: sort ids by (length asc, id asc) (R11), rank i takes sorted
+ *     positions i, i+W, i+2W, ... in that order (R12).
+ *   UB_BAL_SNAKE: same sort, round r dealt to ranks 0..W-1 (r even) or W-1..0 (r odd).
+ *   UB_BAL_EXACT_SMALL: exhaustive min-max search over equal-cardinality partitions,
+ *     W*B <= 12 else UB_ERR_UNSUPPORTED; ties -> lexicographically smallest perm (R15).
+ * Outputs (host, caller-allocated):
+ *   h_perm [W*B]         perm[r*B + k] = global id of the k-th sample placed on rank r
+ *   h_rank_tokens [W]    tokens per rank after the exchange (may be NULL)
+ *   h_send_samples [W*W] samples moving src -> dst, index src*W + dst (may be NULL)
+ *   h_send_tokens [W*W]  tokens moving src -> dst (may be NULL)
+ * Errors: W < 1, B < 1, a length < 1 -> INVALID_ARG; length > max_seqlen -> CAPACITY.
+ */
+typedef enum { UB_BAL_PAPER = 0, UB_BAL_SNAKE = 1, UB_BAL_EXACT_SMALL = 2 } ub_bal_mode;
+
+ub_status ub_balance_plan(const int32_t* h_all_lengths, int32_t W, int32_t B, int32_t max_seqlen,
+                          int32_t mode, int32_t* h_perm, int64_t* h_rank_tokens,
+                          int32_t* h_send_samples, int64_t* h_send_tokens);
+
+/* ------------------------------------------------------------------------------------
+ * Exchange data movement (P:355-359 steps 1 and 3, without the padded all-gather: only
+ * lengths are all-gathered; each sample's packed token records then travel once).
+ *
+ * ub_exchange_tables (host): copy table for rank `rank`, from the all-gathered lengths
+ * and the plan.  h_tab [5*B] int64 = {src_tok[B], len[B], dst_tok[B], src_smp[B], dst_smp[B]}
+ * (token offsets in records, sample offsets in records).
+ *   is_unpack == 0 (pack): source = this rank's packed batch (sample k at its cu[k]);
+ *     destination = the send buffer, grouped by destination rank ascending, each group
+ *     in the destination's perm order.  h_counts [W] (may be NULL) = token records sent
+ *     to each destination; h_scounts [W] = samples sent to each destination.
+ *   is_unpack == 1 (unpack): source = the receive buffer (per-source chunks, source rank
+ *     ascending, each chunk in this rank's perm order); destination = perm order.
+ *     h_counts [W] = token records received from each source; h_scounts [W] samples.
+ *   *h_total_tokens (may be NULL) = tokens packed (pack) / received (unpack).
+ * ub_exchange_copy (device): for each of the B table entries copies len*rec_bytes from
+ *   src_tokens + src_tok*rec_bytes to dst_tokens + dst_tok*rec_bytes and srec_bytes from
+ *   src_samples + src_smp*srec_bytes to dst_samples + dst_smp*srec_bytes.  d_tab is the
+ *   table in device memory.  srec_bytes may be 0 (then sample pointers may be NULL).
+ */
+ub_status ub_exchange_tables(const int32_t* h_all_lengths, const int32_t* h_perm, int32_t W,
+                             int32_t B, int32_t rank, int32_t is_unpack, int64_t* h_tab,
+                             int64_t* h_counts, int64_t* h_scounts, int64_t* h_total_tokens);
+ub_status ub_exchange_copy(const void* src_tokens, void* dst_tokens, const void* src_samples,
+                           void* dst_samples, const int64_t* d_tab, int32_t B, int64_t rec_bytes,
+                           int64_t srec_bytes, void* stream);
+
+/* NCCL communicator (NCCL over NVLink 5 / NVSwitch).  nccl_unique_id: the 128-byte
+ * ncclUniqueId produced by ub_comm_unique_id() on rank 0 and broadcast by the caller
+ * (e.g. over a torch.distributed process group).  Must be called with the CUDA device
+ * of this rank current. */
+ub_status ub_comm_unique_id(void* out_id_128);
+ub_status ub_comm_init(void** out_comm, const void* nccl_unique_id, int32_t W, int32_t rank);
+ub_status ub_comm_destroy(void* comm);
+
+/* All-gather of B int32 lengths (P:355 step 1, lengths only): d_my_lengths [B] ->
+ * d_all_lengths [W*B] rank-major, on `stream`. */
+ub_status ub_allgather_lengths(void* comm, const int32_t* d_my_lengths, int32_t* d_all_lengths,
+                               int32_t B, void* stream);
+
+/* The whole exchange for one step, on `side_stream` (one mini-batch ahead,
+ * overlapped with the compute stream):
+ *   1. all-gather lengths (NCCL), 2. D2H of the W*B lengths and a host wait on the side
+ *   stream only (send/recv counts must be known on the host -- the single host sync of
+ *   the library; it never waits on the compute stream), 3. ub_balance_plan, 4. pack,
+ *   5. grouped ncclSend/ncclRecv (all-to-all-v of packed token records and sample
+ *   records), 6. unpack into perm order, 7. H2D of the new cu_seqlens.
+ * Inputs: d_my_lengths [B]; d_my_tokens [T_mine, rec]; d_my_samples [B, srec].
+ * Outputs: d_out_tokens [capacity_tokens, rec]; d_out_samples [B, srec]; d_out_cu [B+1];
+ *   h_perm [W*B] (may be NULL); *h_out_T.  Capacity: out tokens must fit
+ *   capacity_tokens (else UB_ERR_CAPACITY, nothing moved).
+ * ws: device workspace of ub_exchange_workspace_bytes(W, B, capacity_tokens, rec, srec).
+ */
+size_t ub_exchange_workspace_bytes(int32_t W, int32_t B, int64_t capacity_tokens, int64_t rec_bytes,
+                                   int64_t srec_bytes);
+ub_status ub_balance_exchange(void* comm, int32_t mode, int32_t B, int32_t max_seqlen,
+                              const int32_t* d_my_lengths, const void* d_my_tokens,
+                              const void* d_my_samples, int64_t rec_bytes, int64_t srec_bytes,
+                              int64_t capacity_tokens, void* d_out_tokens, void* d_out_samples,
+                              int32_t* d_out_cu, int32_t* h_perm, int64_t* h_out_T, void* ws,
+                              void* side_stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* UB_H_ */

@@ -135,39 +135,42 @@ def attention_probs(q, k, lengths, scale):
     return out
 
 
-def _keep_fn(offsets, seed, offset, p):
+def _keep_fn(offsets, seed, offset, p, t_base=0):
     def keep(b, h):
         L = int(offsets[b + 1] - offsets[b])
-        return philox.keep_mask_block(seed, offset, int(offsets[b]), L, h, p)
+        return philox.keep_mask_block(seed, offset, t_base + int(offsets[b]), L, h, p)
     return keep
 
 
-def varlen_fwd(qkv, offsets, max_seq_len, scale, p=0.0, seed=0, offset=0):
+def varlen_fwd(qkv, offsets, max_seq_len, scale, p=0.0, seed=0, offset=0, t_base=0):
     """The library's forward contract on packed inputs, via pad -> padded-masked -> unpad.
 
     qkv: [T, 3, H, D] (any float dtype; computed in float64).  offsets = batch_offset.
+    t_base: packed-row index of qkv[0] in the full batch (dropout coordinates are
+    absolute rows, R5), so a slice of sequences can be checked on its own.
     Returns O [T, H, D] and LSE [H, T] (natural log), both float64.
     """
     qkv = np.asarray(qkv, dtype=np.float64)
     lengths = np.diff(np.asarray(offsets))
     padded = varlen.pad(qkv, offsets, max_seq_len, 0.0)          # [B, S, 3, H, D]
     q, k, v = padded[:, :, 0], padded[:, :, 1], padded[:, :, 2]
-    keep = _keep_fn(offsets, seed, offset, p) if p > 0.0 else None
+    keep = _keep_fn(offsets, seed, offset, p, t_base) if p > 0.0 else None
     O, LSE = mha_fwd_padded(q, k, v, lengths, scale, p, keep)
     O_packed = varlen.unpad(O, lengths)
     LSE_packed = varlen.unpad(np.transpose(LSE, (0, 2, 1)), lengths)  # [T, H]
     return O_packed, np.ascontiguousarray(LSE_packed.T)
 
 
-def varlen_bwd(qkv, dout, offsets, max_seq_len, scale, p=0.0, seed=0, offset=0):
-    """Backward contract on packed inputs.  Returns dqkv [T, 3, H, D] float64."""
+def varlen_bwd(qkv, dout, offsets, max_seq_len, scale, p=0.0, seed=0, offset=0, t_base=0):
+    """Backward contract on packed inputs (t_base as in varlen_fwd).  Returns dqkv
+    [T, 3, H, D] float64."""
     qkv = np.asarray(qkv, dtype=np.float64)
     dout = np.asarray(dout, dtype=np.float64)
     lengths = np.diff(np.asarray(offsets))
     padded = varlen.pad(qkv, offsets, max_seq_len, 0.0)
     dO = varlen.pad(dout, offsets, max_seq_len, 0.0)
     q, k, v = padded[:, :, 0], padded[:, :, 1], padded[:, :, 2]
-    keep = _keep_fn(offsets, seed, offset, p) if p > 0.0 else None
+    keep = _keep_fn(offsets, seed, offset, p, t_base) if p > 0.0 else None
     dQ, dK, dV = mha_bwd_padded(q, k, v, dO, lengths, scale, p, keep)
     d = np.stack([dQ, dK, dV], axis=2)                          # [B, S, 3, H, D]
     return varlen.unpad(d, lengths)

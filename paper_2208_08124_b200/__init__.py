@@ -1,0 +1,13 @@
+"""Unpadded-BERT data-parallel hot path for NVIDIA B200 (sm_100a).
+
+arXiv 2208.08124 ("Boosting Distributed Training Performance of the Unpadded BERT
+Model"): unpad/pad gather-scatter, varlen fused multi-head attention forward
+and backward grouped by length, and the padding-exchange load
+balancer.  The compute lives in libub.so (include/ub.h); this package is
+its argument-marshalling binding.
+"""
+from .api import (Comm, balance_plan, cu_seqlens, exchange_copy, exchange_tables, lengths_from_mask, pad, unpad,
+                  varlen_fmha_bwd, varlen_fmha_fwd, version)
+
+__all__ = ["Comm", "balance_plan", "cu_seqlens", "exchange_copy", "exchange_tables", "lengths_from_mask", "pad",
+           "unpad", "varlen_fmha_bwd", "varlen_fmha_fwd", "version"]

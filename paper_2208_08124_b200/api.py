@@ -1,0 +1,218 @@
+"""Thin Python binding of include/ub.h -- argument marshalling only.
+
+Every step of the hot path runs inside libub.so (hand-written sm_100a CUDA + NCCL);
+PyTorch only supplies device memory, streams and process groups.  Names follow the C
+ABI (and the paper's vocabulary: batch_offset == cu_seqlens).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from ._lib import (UB_BAL_EXACT_SMALL, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BF16, UB_FP32, FmhaParams, check, lib)
+
+BAL_MODES = {"paper": UB_BAL_PAPER, "snake": UB_BAL_SNAKE, "exact_small": UB_BAL_EXACT_SMALL}
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _np_ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+_ws_cache = {}
+
+
+def _workspace(nbytes: int, device, tag: str) -> torch.Tensor:
+    key = (tag, str(device))
+    buf = _ws_cache.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = buf
+    return buf
+
+
+def version() -> str:
+    return lib().ub_version().decode()
+
+
+# ------------------------------------------------------------------ batch_offset
+def cu_seqlens(lengths, max_seqlen: int) -> np.ndarray:
+    """Host prefix sum with validation; returns int32 [B+1]."""
+    L = np.ascontiguousarray(np.asarray(lengths, dtype=np.int32))
+    out = np.zeros(L.size + 1, dtype=np.int32)
+    check(lib().ub_cu_seqlens(_np_ptr(L), L.size, int(max_seqlen), _np_ptr(out)))
+    return out
+
+
+def lengths_from_mask(mask) -> np.ndarray:
+    m = np.ascontiguousarray(np.asarray(mask, dtype=np.int32))
+    out = np.zeros(m.shape[0], dtype=np.int32)
+    check(lib().ub_lengths_from_mask(_np_ptr(m), m.shape[0], m.shape[1], _np_ptr(out)))
+    return out
+
+
+# ------------------------------------------------------------------ unpad / pad
+def unpad(padded: torch.Tensor, cu: torch.Tensor, T: int, out: torch.Tensor | None = None, stream=None):
+    """Gather: padded [B, S, *row] -> packed [T, *row]."""
+    B, S = padded.shape[0], padded.shape[1]
+    row_bytes = padded[0, 0].numel() * padded.element_size()
+    if out is None:
+        out = torch.empty((T,) + tuple(padded.shape[2:]), dtype=padded.dtype, device=padded.device)
+    check(lib().ub_unpad(_ptr(padded), _ptr(out), _ptr(cu), B, S, int(T), row_bytes, _stream(stream)))
+    return out
+
+
+def pad(packed: torch.Tensor, cu: torch.Tensor, B: int, S: int, pad_row: torch.Tensor | None = None,
+        out: torch.Tensor | None = None, stream=None):
+    """Scatter: packed [T, *row] -> padded [B, S, *row] (pad_row or zeros elsewhere)."""
+    T = packed.shape[0]
+    row_bytes = packed[0].numel() * packed.element_size() if T > 0 else \
+        int(np.prod(packed.shape[1:])) * packed.element_size()
+    if out is None:
+        out = torch.empty((B, S) + tuple(packed.shape[1:]), dtype=packed.dtype, device=packed.device)
+    check(lib().ub_pad(_ptr(packed), _ptr(out), _ptr(cu), B, S, int(T), row_bytes, _ptr(pad_row), _stream(stream)))
+    return out
+
+
+# ------------------------------------------------------------------ varlen FMHA
+def fmha_params(B, T, max_seqlen, heads, head_dim, dtype, scale=None, p_dropout=0.0, seed=0, offset=0):
+    return FmhaParams(B=int(B), T=int(T), max_seqlen=int(max_seqlen), heads=int(heads), head_dim=int(head_dim),
+                      scale=float(scale if scale is not None else 1.0 / math.sqrt(head_dim)),
+                      p_dropout=float(p_dropout), seed=int(seed), offset=int(offset),
+                      dtype=UB_BF16 if dtype == torch.bfloat16 else UB_FP32)
+
+
+def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=None, p_dropout=0.0, seed=0,
+                    offset=0, out=None, lse=None, stream=None):
+    """Eq. (1) over packed qkv [T, 3, H, D]; returns (out [T,H,D], lse [H,T] fp32)."""
+    T, three, H, D = qkv.shape
+    assert three == 3
+    B = cu.numel() - 1
+    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset)
+    if out is None:
+        out = torch.empty((T, H, D), dtype=qkv.dtype, device=qkv.device)
+    if lse is None:
+        lse = torch.empty((H, T), dtype=torch.float32, device=qkv.device)
+    ws = _workspace(lib().ub_fmha_workspace_bytes(C.byref(prm), 0), qkv.device, "fmha_fwd")
+    check(lib().ub_varlen_fmha_fwd(C.byref(prm), _ptr(qkv), _ptr(cu), _ptr(out), _ptr(lse), _ptr(ws),
+                                   _stream(stream)))
+    return out, lse
+
+
+def varlen_fmha_bwd(qkv, out, lse, dout, cu, max_seqlen: int, scale=None, p_dropout=0.0, seed=0, offset=0,
+                    dqkv=None, stream=None):
+    """Backward of varlen_fmha_fwd; returns dqkv [T, 3, H, D]."""
+    T, _, H, D = qkv.shape
+    B = cu.numel() - 1
+    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset)
+    if dqkv is None:
+        dqkv = torch.empty_like(qkv)
+    ws = _workspace(lib().ub_fmha_workspace_bytes(C.byref(prm), 1), qkv.device, "fmha_bwd")
+    check(lib().ub_varlen_fmha_bwd(C.byref(prm), _ptr(qkv), _ptr(out), _ptr(lse), _ptr(dout), _ptr(cu),
+                                   _ptr(dqkv), _ptr(ws), _stream(stream)))
+    return dqkv
+
+
+# ------------------------------------------------------------------ balancer
+def balance_plan(all_lengths, W: int, B: int, max_seqlen: int, mode: str = "paper") -> dict:
+    """Host planner: perm, rank_tokens, send_samples [W*W], send_tokens [W*W]."""
+    a = np.ascontiguousarray(np.asarray(all_lengths, dtype=np.int32).reshape(-1))
+    perm = np.zeros(W * B, dtype=np.int32)
+    rt = np.zeros(W, dtype=np.int64)
+    ss = np.zeros(W * W, dtype=np.int32)
+    st = np.zeros(W * W, dtype=np.int64)
+    check(lib().ub_balance_plan(_np_ptr(a), W, B, int(max_seqlen), BAL_MODES[mode], _np_ptr(perm), _np_ptr(rt),
+                                _np_ptr(ss), _np_ptr(st)))
+    return {"perm": perm, "rank_tokens": rt, "send_samples": ss, "send_tokens": st}
+
+
+def exchange_tables(all_lengths, perm, W: int, B: int, rank: int, unpack: bool):
+    a = np.ascontiguousarray(np.asarray(all_lengths, dtype=np.int32).reshape(-1))
+    p = np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    tab = np.zeros(5 * B, dtype=np.int64)
+    counts = np.zeros(W, dtype=np.int64)
+    scounts = np.zeros(W, dtype=np.int64)
+    total = np.zeros(1, dtype=np.int64)
+    check(lib().ub_exchange_tables(_np_ptr(a), _np_ptr(p), W, B, rank, int(unpack), _np_ptr(tab), _np_ptr(counts),
+                                   _np_ptr(scounts), _np_ptr(total)))
+    return tab, counts, scounts, int(total[0])
+
+
+def exchange_copy(src_tokens, dst_tokens, src_samples, dst_samples, d_tab, B, rec_bytes, srec_bytes, stream=None):
+    check(lib().ub_exchange_copy(_ptr(src_tokens), _ptr(dst_tokens), _ptr(src_samples), _ptr(dst_samples),
+                                 _ptr(d_tab), B, int(rec_bytes), int(srec_bytes), _stream(stream)))
+
+
+class Comm:
+    """NCCL communicator owned by the library (ub_comm).  Bootstrap: rank 0 creates the
+    unique id, the caller broadcasts it over a torch.distributed group."""
+
+    def __init__(self, world: int, rank: int, group=None):
+        import torch.distributed as dist
+        idbuf = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            raw = (C.c_uint8 * 128)()
+            check(lib().ub_comm_unique_id(C.cast(raw, C.c_void_p)))
+            idbuf = torch.tensor(list(bytes(raw)), dtype=torch.uint8)
+        if world > 1:
+            dev_buf = idbuf.cuda() if dist.get_backend(group) == "nccl" else idbuf
+            dist.broadcast(dev_buf, 0, group=group)
+            idbuf = dev_buf.cpu()
+        raw = (C.c_uint8 * 128)(*idbuf.tolist())
+        h = C.c_void_p()
+        check(lib().ub_comm_init(C.byref(h), C.cast(raw, C.c_void_p), world, rank))
+        self.handle, self.world, self.rank = h, world, rank
+
+    def allgather_lengths(self, d_lengths: torch.Tensor, out=None, stream=None):
+        B = d_lengths.numel()
+        if out is None:
+            out = torch.empty(self.world * B, dtype=torch.int32, device=d_lengths.device)
+        check(lib().ub_allgather_lengths(self.handle, _ptr(d_lengths), _ptr(out), B, _stream(stream)))
+        return out
+
+    def balance_exchange(self, d_lengths, d_tokens, d_samples, capacity_tokens, max_seqlen, mode="paper",
+                         out_tokens=None, out_samples=None, out_cu=None, stream=None):
+        """One step of the exchange on `stream`.  Returns
+        (out_tokens, out_samples, out_cu, T_out, perm)."""
+        B = d_lengths.numel()
+        rec = d_tokens[0].numel() * d_tokens.element_size() if d_tokens.shape[0] else \
+            int(np.prod(d_tokens.shape[1:])) * d_tokens.element_size()
+        srec = d_samples[0].numel() * d_samples.element_size() if d_samples is not None else 0
+        dev = d_lengths.device
+        if out_tokens is None:
+            out_tokens = torch.empty((capacity_tokens,) + tuple(d_tokens.shape[1:]), dtype=d_tokens.dtype, device=dev)
+        if out_samples is None and d_samples is not None:
+            out_samples = torch.empty_like(d_samples)
+        if out_cu is None:
+            out_cu = torch.empty(B + 1, dtype=torch.int32, device=dev)
+        ws = _workspace(lib().ub_exchange_workspace_bytes(self.world, B, capacity_tokens, rec, srec), dev,
+                        f"exchange{self.rank}")
+        perm = np.zeros(self.world * B, dtype=np.int32)
+        T_out = C.c_int64(0)
+        check(lib().ub_balance_exchange(self.handle, BAL_MODES[mode], B, int(max_seqlen), _ptr(d_lengths),
+                                        _ptr(d_tokens), _ptr(d_samples), rec, srec, int(capacity_tokens),
+                                        _ptr(out_tokens), _ptr(out_samples), _ptr(out_cu), _np_ptr(perm),
+                                        C.byref(T_out), _ptr(ws), _stream(stream)))
+        return out_tokens, out_samples, out_cu, int(T_out.value), perm
+
+    def close(self):
+        if self.handle:
+            check(lib().ub_comm_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

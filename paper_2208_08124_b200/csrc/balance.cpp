@@ -1,0 +1,180 @@
+// Host-side padding-exchange planner (§IV-B-1) and exchange copy tables.
+// Pure functions of the all-gathered lengths: every rank computes byte-identical output.
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "ub_internal.h"
+
+namespace ub {
+namespace {
+
+// Step 2: order global ids by (valid tokens asc, id asc) -- R11.
+std::vector<int32_t> sorted_ids(const int32_t* a, int32_t n) {
+  std::vector<int32_t> ids(n);
+  std::iota(ids.begin(), ids.end(), 0);
+  std::stable_sort(ids.begin(), ids.end(), [a](int32_t x, int32_t y) { return a[x] < a[y]; });
+  return ids;
+}
+
+struct ExactSearch {  // exhaustive min-max partition search for W*B <= 12 (R15 (iii))
+  const int32_t* a;
+  int32_t W, B, n;
+  std::vector<std::vector<int32_t>> cur, best_groups;
+  int64_t best_val = -1;
+  std::vector<int32_t> best_perm;
+
+  void canon(std::vector<int32_t>& g) const {
+    std::sort(g.begin(), g.end(), [this](int32_t x, int32_t y) { return a[x] != a[y] ? a[x] < a[y] : x < y; });
+  }
+  void evaluate() {
+    int64_t val = 0;
+    for (auto& g : cur) {
+      int64_t s = 0;
+      for (int32_t x : g) s += a[x];
+      val = std::max(val, s);
+    }
+    if (best_val >= 0 && val > best_val) return;
+    std::vector<std::vector<int32_t>> groups = cur;
+    for (auto& g : groups) canon(g);
+    std::sort(groups.begin(), groups.end());
+    std::vector<int32_t> perm;
+    for (auto& g : groups) perm.insert(perm.end(), g.begin(), g.end());
+    if (best_val < 0 || val < best_val || perm < best_perm) {
+      best_val = val;
+      best_perm = perm;
+      best_groups = groups;
+    }
+  }
+  // take the smallest remaining id, choose its B-1 companions, recurse
+  void rec(std::vector<int32_t>& rem) {
+    if (rem.empty()) { evaluate(); return; }
+    const int32_t first = rem[0];
+    std::vector<int32_t> rest(rem.begin() + 1, rem.end());
+    const int m = (int)rest.size(), k = B - 1;
+    std::vector<int> idx(k);
+    std::iota(idx.begin(), idx.end(), 0);
+    while (true) {
+      std::vector<int32_t> grp{first};
+      std::vector<char> used(m, 0);
+      for (int j : idx) { grp.push_back(rest[j]); used[j] = 1; }
+      std::vector<int32_t> left;
+      for (int j = 0; j < m; ++j) if (!used[j]) left.push_back(rest[j]);
+      cur.push_back(grp);
+      rec(left);
+      cur.pop_back();
+      // next combination
+      int i = k - 1;
+      while (i >= 0 && idx[i] == m - k + i) --i;
+      if (i < 0) break;
+      ++idx[i];
+      for (int j = i + 1; j < k; ++j) idx[j] = idx[j - 1] + 1;
+    }
+  }
+};
+
+}  // namespace
+}  // namespace ub
+
+using namespace ub;
+
+extern "C" ub_status ub_balance_plan(const int32_t* a, int32_t W, int32_t B, int32_t max_seqlen, int32_t mode,
+                                     int32_t* perm, int64_t* rank_tokens, int32_t* send_samples,
+                                     int64_t* send_tokens) {
+  clear_error();
+  UB_REQUIRE(a && perm, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(W >= 1 && B >= 1, UB_ERR_INVALID_ARG, "W=%d B=%d", W, B);
+  UB_REQUIRE((int64_t)W * B <= (1 << 30), UB_ERR_SHAPE, "W*B too large");
+  const int32_t n = W * B;
+  for (int32_t g = 0; g < n; ++g) {
+    UB_REQUIRE(a[g] >= 1, UB_ERR_INVALID_ARG, "length[%d] = %d < 1", g, a[g]);
+    UB_REQUIRE(a[g] <= max_seqlen, UB_ERR_CAPACITY, "length[%d] = %d > max_seqlen %d", g, a[g], max_seqlen);
+  }
+  if (mode == UB_BAL_PAPER) {
+    const auto ids = sorted_ids(a, n);
+    for (int32_t i = 0; i < W; ++i)                 // worker i takes i, i+W, i+2W, ...
+      for (int32_t k = 0; k < B; ++k) perm[i * B + k] = ids[i + k * W];
+  } else if (mode == UB_BAL_SNAKE) {
+    const auto ids = sorted_ids(a, n);
+    for (int32_t r = 0; r < B; ++r)
+      for (int32_t s = 0; s < W; ++s) {
+        const int32_t dst = (r % 2 == 0) ? s : W - 1 - s;
+        perm[dst * B + r] = ids[r * W + s];
+      }
+  } else if (mode == UB_BAL_EXACT_SMALL) {
+    UB_REQUIRE(n <= 12, UB_ERR_UNSUPPORTED, "UB_BAL_EXACT_SMALL needs W*B <= 12 (got %d)", n);
+    ExactSearch es{a, W, B, n};
+    std::vector<int32_t> rem(n);
+    std::iota(rem.begin(), rem.end(), 0);
+    es.rec(rem);
+    for (int32_t i = 0; i < n; ++i) perm[i] = es.best_perm[i];
+  } else {
+    return set_error(UB_ERR_INVALID_ARG, "bad balance mode %d", mode);
+  }
+  if (rank_tokens)
+    for (int32_t r = 0; r < W; ++r) {
+      int64_t t = 0;
+      for (int32_t k = 0; k < B; ++k) t += a[perm[r * B + k]];
+      rank_tokens[r] = t;
+    }
+  if (send_samples) std::fill(send_samples, send_samples + (int64_t)W * W, 0);
+  if (send_tokens) std::fill(send_tokens, send_tokens + (int64_t)W * W, 0);
+  for (int32_t dst = 0; dst < W; ++dst)
+    for (int32_t k = 0; k < B; ++k) {
+      const int32_t g = perm[dst * B + k], src = g / B;
+      if (send_samples) send_samples[src * W + dst] += 1;
+      if (send_tokens) send_tokens[src * W + dst] += a[g];
+    }
+  return UB_OK;
+}
+
+extern "C" ub_status ub_exchange_tables(const int32_t* a, const int32_t* perm, int32_t W, int32_t B, int32_t rank,
+                                        int32_t is_unpack, int64_t* tab, int64_t* counts, int64_t* scounts,
+                                        int64_t* total_tokens) {
+  clear_error();
+  UB_REQUIRE(a && perm && tab, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(W >= 1 && B >= 1 && rank >= 0 && rank < W, UB_ERR_INVALID_ARG, "bad W/B/rank");
+  int64_t* src_tok = tab;
+  int64_t* len = tab + B;
+  int64_t* dst_tok = tab + 2 * B;
+  int64_t* src_smp = tab + 3 * B;
+  int64_t* dst_smp = tab + 4 * B;
+  std::vector<int64_t> cnt(W, 0), scnt(W, 0);
+  if (!is_unpack) {
+    // source: this rank's packed batch; cu of local samples
+    std::vector<int64_t> cu(B + 1, 0);
+    for (int32_t k = 0; k < B; ++k) cu[k + 1] = cu[k] + a[rank * B + k];
+    int64_t off = 0;
+    int32_t q = 0;
+    for (int32_t dst = 0; dst < W; ++dst)
+      for (int32_t k = 0; k < B; ++k) {
+        const int32_t g = perm[dst * B + k];
+        if (g / B != rank) continue;
+        const int32_t kk = g % B;
+        UB_REQUIRE(q < B, UB_ERR_SHAPE, "perm is not a permutation");
+        src_tok[q] = cu[kk]; len[q] = a[g]; dst_tok[q] = off; src_smp[q] = kk; dst_smp[q] = q;
+        off += a[g]; cnt[dst] += a[g]; scnt[dst] += 1; ++q;
+      }
+    UB_REQUIRE(q == B, UB_ERR_SHAPE, "rank %d sends %d samples, expected %d", rank, q, B);
+    if (total_tokens) *total_tokens = off;
+  } else {
+    // receive buffer: chunks per source rank ascending, each in this rank's perm order
+    for (int32_t k = 0; k < B; ++k) {
+      const int32_t g = perm[rank * B + k];
+      cnt[g / B] += a[g];
+      scnt[g / B] += 1;
+    }
+    std::vector<int64_t> base(W, 0), sbase(W, 0);
+    for (int32_t s = 1; s < W; ++s) { base[s] = base[s - 1] + cnt[s - 1]; sbase[s] = sbase[s - 1] + scnt[s - 1]; }
+    int64_t off = 0;
+    for (int32_t k = 0; k < B; ++k) {
+      const int32_t g = perm[rank * B + k], s = g / B;
+      src_tok[k] = base[s]; len[k] = a[g]; dst_tok[k] = off; src_smp[k] = sbase[s]; dst_smp[k] = k;
+      base[s] += a[g]; sbase[s] += 1; off += a[g];
+    }
+    if (total_tokens) *total_tokens = off;
+  }
+  if (counts) for (int32_t r = 0; r < W; ++r) counts[r] = cnt[r];
+  if (scounts) for (int32_t r = 0; r < W; ++r) scounts[r] = scnt[r];
+  return UB_OK;
+}

@@ -1,0 +1,205 @@
+// Cross-rank token rebalancing over NCCL (NVLink 5 / NVSwitch): all-gather of the valid
+// lengths + all-to-all-v of packed samples, replacing the paper's all-gather of five
+// padded tensors and its CPU/MPI variant.
+//
+// Only lengths cross the fabric before the plan is known (W*B int32); each sample's
+// token records then move exactly once (P:359's slice is realised as a grouped
+// ncclSend/ncclRecv phase).  Everything is enqueued on the caller's side stream so that
+// step n+1's exchange overlaps step n's compute.
+#include <nccl.h>
+
+#include <cstring>
+#include <vector>
+
+#include "ub_internal.h"
+
+namespace ub {
+
+struct Comm {
+  ncclComm_t nccl = nullptr;
+  int32_t W = 0, rank = 0;
+  // pinned host staging (reused across calls; every call synchronises the side stream
+  // before rewriting it)
+  int32_t* h_all = nullptr;
+  int64_t* h_tab_pack = nullptr;
+  int64_t* h_tab_unpack = nullptr;
+  int32_t* h_cu = nullptr;
+  int32_t cap_B = 0;
+};
+
+#define UB_CHECK_NCCL(expr)                                                                  \
+  do {                                                                                       \
+    ncclResult_t r_ = (expr);                                                                \
+    if (r_ != ncclSuccess)                                                                   \
+      return ::ub::set_error(UB_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_));          \
+  } while (0)
+
+static ub_status ensure_staging(Comm* c, int32_t B) {
+  if (c->cap_B >= B) return UB_OK;
+  cudaFreeHost(c->h_all);
+  cudaFreeHost(c->h_tab_pack);
+  cudaFreeHost(c->h_tab_unpack);
+  cudaFreeHost(c->h_cu);
+  c->h_all = nullptr; c->h_tab_pack = nullptr; c->h_tab_unpack = nullptr; c->h_cu = nullptr; c->cap_B = 0;
+  UB_CHECK_CUDA(cudaMallocHost(&c->h_all, sizeof(int32_t) * (size_t)c->W * B));
+  UB_CHECK_CUDA(cudaMallocHost(&c->h_tab_pack, sizeof(int64_t) * 5 * (size_t)B));
+  UB_CHECK_CUDA(cudaMallocHost(&c->h_tab_unpack, sizeof(int64_t) * 5 * (size_t)B));
+  UB_CHECK_CUDA(cudaMallocHost(&c->h_cu, sizeof(int32_t) * ((size_t)B + 1)));
+  c->cap_B = B;
+  return UB_OK;
+}
+
+struct ExWs {  // carve-up of the exchange workspace
+  int32_t* all_lengths; int64_t* tab_pack; int64_t* tab_unpack;
+  uint8_t* send_tok; uint8_t* recv_tok; uint8_t* send_smp; uint8_t* recv_smp;
+};
+static size_t ex_layout(int32_t W, int32_t B, int64_t cap, int64_t rec, int64_t srec, void* base, ExWs* out) {
+  size_t off = 0;
+  auto take = [&](size_t n) { size_t o = off; off = align_up(off + n, 256); return o; };
+  const size_t o_all = take(sizeof(int32_t) * (size_t)W * B);
+  const size_t o_tp = take(sizeof(int64_t) * 5 * (size_t)B);
+  const size_t o_tu = take(sizeof(int64_t) * 5 * (size_t)B);
+  const size_t o_st = take((size_t)cap * rec);
+  const size_t o_rt = take((size_t)cap * rec);
+  const size_t o_ss = take((size_t)B * srec);
+  const size_t o_rs = take((size_t)B * srec);
+  if (out && base) {
+    char* b = static_cast<char*>(base);
+    out->all_lengths = reinterpret_cast<int32_t*>(b + o_all);
+    out->tab_pack = reinterpret_cast<int64_t*>(b + o_tp);
+    out->tab_unpack = reinterpret_cast<int64_t*>(b + o_tu);
+    out->send_tok = reinterpret_cast<uint8_t*>(b + o_st);
+    out->recv_tok = reinterpret_cast<uint8_t*>(b + o_rt);
+    out->send_smp = reinterpret_cast<uint8_t*>(b + o_ss);
+    out->recv_smp = reinterpret_cast<uint8_t*>(b + o_rs);
+  }
+  return off;
+}
+
+}  // namespace ub
+
+using namespace ub;
+
+extern "C" ub_status ub_comm_unique_id(void* out_id_128) {
+  clear_error();
+  UB_REQUIRE(out_id_128, UB_ERR_INVALID_ARG, "null pointer");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  UB_CHECK_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out_id_128, &id, sizeof(id));
+  return UB_OK;
+}
+
+extern "C" ub_status ub_comm_init(void** out_comm, const void* id_128, int32_t W, int32_t rank) {
+  clear_error();
+  UB_REQUIRE(out_comm && id_128, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(W >= 1 && rank >= 0 && rank < W, UB_ERR_INVALID_ARG, "bad W/rank");
+  ncclUniqueId id;
+  std::memcpy(&id, id_128, sizeof(id));
+  Comm* c = new Comm();
+  c->W = W;
+  c->rank = rank;
+  ncclResult_t r = ncclCommInitRank(&c->nccl, W, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return set_error(UB_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  *out_comm = c;
+  return UB_OK;
+}
+
+extern "C" ub_status ub_comm_destroy(void* comm) {
+  clear_error();
+  if (!comm) return UB_OK;
+  Comm* c = static_cast<Comm*>(comm);
+  if (c->nccl) ncclCommDestroy(c->nccl);
+  cudaFreeHost(c->h_all);
+  cudaFreeHost(c->h_tab_pack);
+  cudaFreeHost(c->h_tab_unpack);
+  cudaFreeHost(c->h_cu);
+  delete c;
+  return UB_OK;
+}
+
+extern "C" ub_status ub_allgather_lengths(void* comm, const int32_t* d_my, int32_t* d_all, int32_t B, void* stream) {
+  clear_error();
+  UB_REQUIRE(comm && d_my && d_all && B >= 1, UB_ERR_INVALID_ARG, "bad args");
+  Comm* c = static_cast<Comm*>(comm);
+  UB_CHECK_NCCL(ncclAllGather(d_my, d_all, (size_t)B, ncclInt32, c->nccl, as_stream(stream)));
+  return UB_OK;
+}
+
+extern "C" size_t ub_exchange_workspace_bytes(int32_t W, int32_t B, int64_t cap, int64_t rec, int64_t srec) {
+  if (W < 1 || B < 1 || cap < 0 || rec < 0 || srec < 0) return 0;
+  return ex_layout(W, B, cap, rec, srec, nullptr, nullptr);
+}
+
+extern "C" ub_status ub_balance_exchange(void* comm, int32_t mode, int32_t B, int32_t max_seqlen,
+                                         const int32_t* d_my_lengths, const void* d_my_tokens,
+                                         const void* d_my_samples, int64_t rec, int64_t srec, int64_t cap,
+                                         void* d_out_tokens, void* d_out_samples, int32_t* d_out_cu,
+                                         int32_t* h_perm, int64_t* h_out_T, void* ws, void* side_stream) {
+  clear_error();
+  UB_REQUIRE(comm && d_my_lengths && d_my_tokens && d_out_tokens && d_out_cu && h_out_T && ws, UB_ERR_INVALID_ARG,
+             "null pointer");
+  UB_REQUIRE(B >= 1 && rec > 0 && srec >= 0 && cap >= 1, UB_ERR_SHAPE, "bad sizes");
+  UB_REQUIRE(srec == 0 || (d_my_samples && d_out_samples), UB_ERR_INVALID_ARG, "null sample pointer");
+  Comm* c = static_cast<Comm*>(comm);
+  const int32_t W = c->W, me = c->rank;
+  cudaStream_t s = as_stream(side_stream);
+  ub_status st = ensure_staging(c, B);
+  if (st != UB_OK) return st;
+  ExWs w;
+  ex_layout(W, B, cap, rec, srec, ws, &w);
+
+  // 1. all-gather of lengths (P:355 step 1, lengths only)
+  UB_CHECK_NCCL(ncclAllGather(d_my_lengths, w.all_lengths, (size_t)B, ncclInt32, c->nccl, s));
+  // 2. lengths to the host: the single host wait, on the side stream only
+  UB_CHECK_CUDA(cudaMemcpyAsync(c->h_all, w.all_lengths, sizeof(int32_t) * (size_t)W * B, cudaMemcpyDeviceToHost, s));
+  UB_CHECK_CUDA(cudaStreamSynchronize(s));
+  // 3. the deterministic plan, identical on every rank
+  std::vector<int32_t> perm((size_t)W * B);
+  if ((st = ub_balance_plan(c->h_all, W, B, max_seqlen, mode, perm.data(), nullptr, nullptr, nullptr)) != UB_OK)
+    return st;
+  std::vector<int64_t> send_cnt(W), send_scnt(W), recv_cnt(W), recv_scnt(W);
+  int64_t T_mine = 0, T_out = 0;
+  if ((st = ub_exchange_tables(c->h_all, perm.data(), W, B, me, 0, c->h_tab_pack, send_cnt.data(), send_scnt.data(),
+                               &T_mine)) != UB_OK)
+    return st;
+  if ((st = ub_exchange_tables(c->h_all, perm.data(), W, B, me, 1, c->h_tab_unpack, recv_cnt.data(),
+                               recv_scnt.data(), &T_out)) != UB_OK)
+    return st;
+  UB_REQUIRE(T_mine <= cap && T_out <= cap, UB_ERR_CAPACITY, "tokens (%lld sent, %lld received) exceed capacity %lld",
+             (long long)T_mine, (long long)T_out, (long long)cap);
+  // 4. pack into destination order
+  UB_CHECK_CUDA(cudaMemcpyAsync(w.tab_pack, c->h_tab_pack, sizeof(int64_t) * 5 * B, cudaMemcpyHostToDevice, s));
+  UB_CHECK_CUDA(cudaMemcpyAsync(w.tab_unpack, c->h_tab_unpack, sizeof(int64_t) * 5 * B, cudaMemcpyHostToDevice, s));
+  if ((st = ub_exchange_copy(d_my_tokens, w.send_tok, d_my_samples, w.send_smp, w.tab_pack, B, rec, srec, s)) != UB_OK)
+    return st;
+  // 5. all-to-all-v over NVLink (grouped point-to-point)
+  UB_CHECK_NCCL(ncclGroupStart());
+  int64_t so = 0, ro = 0, sso = 0, rso = 0;
+  for (int32_t peer = 0; peer < W; ++peer) {
+    if (send_cnt[peer] > 0)
+      UB_CHECK_NCCL(ncclSend(w.send_tok + so * rec, (size_t)(send_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
+    if (recv_cnt[peer] > 0)
+      UB_CHECK_NCCL(ncclRecv(w.recv_tok + ro * rec, (size_t)(recv_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
+    if (srec > 0 && send_scnt[peer] > 0)
+      UB_CHECK_NCCL(ncclSend(w.send_smp + sso * srec, (size_t)(send_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
+    if (srec > 0 && recv_scnt[peer] > 0)
+      UB_CHECK_NCCL(ncclRecv(w.recv_smp + rso * srec, (size_t)(recv_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
+    so += send_cnt[peer]; ro += recv_cnt[peer]; sso += send_scnt[peer]; rso += recv_scnt[peer];
+  }
+  UB_CHECK_NCCL(ncclGroupEnd());
+  // 6. reorder the per-source chunks into perm order (a5)
+  if ((st = ub_exchange_copy(w.recv_tok, d_out_tokens, w.recv_smp, d_out_samples, w.tab_unpack, B, rec, srec, s)) !=
+      UB_OK)
+    return st;
+  // 7. the new cu_seqlens, computed on the host (input-only operators run during the exchange)
+  c->h_cu[0] = 0;
+  for (int32_t k = 0; k < B; ++k) c->h_cu[k + 1] = c->h_cu[k] + c->h_all[perm[(size_t)me * B + k]];
+  UB_CHECK_CUDA(cudaMemcpyAsync(d_out_cu, c->h_cu, sizeof(int32_t) * (B + 1), cudaMemcpyHostToDevice, s));
+  if (h_perm) std::memcpy(h_perm, perm.data(), sizeof(int32_t) * perm.size());
+  *h_out_T = T_out;
+  return UB_OK;
+}

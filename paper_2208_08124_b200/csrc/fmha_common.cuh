@@ -1,0 +1,56 @@
+// Shared pieces of the tcgen05 FMHA kernels: work-item decode, TMA descriptor creation,
+// dropout mask word.
+#pragma once
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include "sm100.cuh"
+#include "ub_internal.h"
+
+namespace ub {
+
+struct WorkItem {
+  int32_t b, h, tile, c0, L, nt;
+};
+
+// Map a flat work index onto (sequence, head, tile) along the bucketed plan.
+__device__ __forceinline__ bool decode_item(int32_t w, const FmhaPlanView& v, const int32_t* __restrict__ cu,
+                                            int32_t B, int32_t H, WorkItem& it) {
+  const int32_t total = v.item_prefix[B];
+  if (w >= total) return false;
+  int32_t lo = 0, hi = B;                       // largest k with prefix[k] <= w
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (v.item_prefix[mid] <= w) lo = mid; else hi = mid - 1;
+  }
+  it.b = v.seq_order[lo];
+  const int32_t local = w - v.item_prefix[lo];
+  it.c0 = cu[it.b];
+  it.L = cu[it.b + 1] - it.c0;
+  it.nt = (it.L + kTile - 1) / kTile;
+  it.h = local / it.nt;
+  it.tile = local - it.h * it.nt;
+  return true;
+}
+
+// Dropout keep bits for 8 consecutive keys j0..j0+7 (j0 % 8 == 0) of packed row t (R5):
+// bit e set <=> key j0+e kept.
+__device__ __forceinline__ uint32_t keep_bits8(uint32_t j0, uint32_t t, uint32_t h, uint32_t off, uint32_t k0,
+                                               uint32_t k1, uint32_t thr) {
+  const U4 w = philox4x32_10(j0 >> 3, t, h, off, k0, k1);
+  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+  uint32_t bits = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t r16 = (words[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+    bits |= (r16 >= thr ? 1u : 0u) << e;
+  }
+  return bits;
+}
+
+// Host: 2-D bf16 tensor map over a row-major [rows, cols] matrix with row pitch
+// `pitch_bytes`, box {64 cols, 128 rows}, 128-B swizzle (matches sdesc_sw128).
+ub_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
+                         uint32_t box_cols = 64, uint32_t box_rows = 128);
+
+}  // namespace ub

@@ -1,0 +1,68 @@
+// Internal helpers shared by the library's translation units (not part of the ABI).
+#pragma once
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "../../include/ub.h"
+
+namespace ub {
+
+ub_status set_error(ub_status st, const char* fmt, ...);
+void clear_error();
+
+// Capability check: device of the current context must be sm_100 (cached per device).
+ub_status require_sm100();
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define UB_CHECK_CUDA(expr)                                                              \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return ::ub::set_error(UB_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                             __FILE__, __LINE__);                                        \
+  } while (0)
+
+#define UB_CHECK_LAUNCH()                                                                \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      return ::ub::set_error(UB_ERR_CUDA, "launch: %s (%s:%d)", cudaGetErrorString(e_),   \
+                             __FILE__, __LINE__);                                        \
+  } while (0)
+
+#define UB_REQUIRE(cond, status, ...)                                                    \
+  do {                                                                                   \
+    if (!(cond)) return ::ub::set_error((status), __VA_ARGS__);                          \
+  } while (0)
+
+// ---- FMHA internals (fmha_*.cu) ------------------------------------------------------
+constexpr int kTile = 128;  // query / key tile (rows) of the tensor-core path and of the plan
+
+struct FmhaPlanView {   // device views into the workspace, filled by the plan kernel
+  int32_t* seq_order;   // [B] sequences sorted by tile count desc (then id asc)
+  int32_t* item_prefix; // [B+1] prefix of items (tiles * H) along seq_order
+  int32_t* counters;    // [4] scheduler counters
+};
+
+size_t fmha_plan_bytes(int32_t B);
+FmhaPlanView fmha_plan_view(void* ws, int32_t B);
+ub_status launch_fmha_plan(const int32_t* d_cu, int32_t B, int32_t H, int32_t max_tiles,
+                           FmhaPlanView v, cudaStream_t s);
+
+ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out,
+                         float* lse, void* ws, cudaStream_t s);
+ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* out, const float* lse,
+                         const void* dout, const int32_t* d_cu, void* dqkv, void* ws, cudaStream_t s);
+size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p);
+
+ub_status fmha_fwd_simt(const ub_fmha_params& p, const float* qkv, const int32_t* d_cu, float* out,
+                        float* lse, cudaStream_t s);
+ub_status fmha_bwd_simt(const ub_fmha_params& p, const float* qkv, const float* out, const float* lse,
+                        const float* dout, const int32_t* d_cu, float* dqkv, float* ws, cudaStream_t s);
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace ub

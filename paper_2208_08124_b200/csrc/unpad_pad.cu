@@ -1,0 +1,154 @@
+// Unpad (gather) and pad (scatter) between padded [B, S, row] and packed
+// [T, row] rows, plus the exchange copy kernel (P:355-359 redistribution).
+//
+// HBM-bound byte movers.  Every thread walks the PADDED index space (B*S rows x V vectors,
+// V = row_bytes / elem) with a grid-stride loop: padded-side accesses are perfectly
+// coalesced, packed-side accesses are contiguous within each row.  Row -> (b, i) uses
+// multiply-high division (no integer divide on the hot loop).  16-B vectors when the
+// row and both base pointers allow it.
+#include "ub_internal.h"
+
+namespace ub {
+
+struct FastDiv {  // q = n / d for 32-bit n (Granlund-Montgomery round-up method)
+  uint32_t d, m, s;
+  __host__ explicit FastDiv(uint32_t d_ = 1) : d(d_) {
+    s = 0;
+    while ((1ull << s) < d) ++s;
+    m = (uint32_t)((((1ull << s) - d) << 32) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)__umulhi(n, m) + n) >> s);
+  }
+};
+
+template <typename Vec, bool kPad>
+__global__ void __launch_bounds__(256) unpad_pad_kernel(const Vec* __restrict__ src, Vec* __restrict__ dst,
+                                                         const int32_t* __restrict__ cu, const Vec* __restrict__ pad_row,
+                                                         uint32_t n, FastDiv divV, FastDiv divS) {
+  constexpr int U = 4;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x + threadIdx.x; base < n; base += stride * U) {
+    Vec val[U];
+    int64_t dst_idx[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t f = base + u * stride;
+      dst_idx[u] = -1;
+      if (f < n) {
+        const uint32_t p = divV.div(f), v = f - p * divV.d;      // padded row p, vector v
+        const uint32_t b = divS.div(p), i = p - b * divS.d;      // sequence b, position i
+        const int32_t c0 = __ldg(cu + b), L = __ldg(cu + b + 1) - c0;
+        const int64_t packed_idx = ((int64_t)c0 + i) * divV.d + v;
+        if constexpr (kPad) {
+          dst_idx[u] = f;
+          if ((int32_t)i < L) val[u] = src[packed_idx];
+          else if (pad_row) val[u] = __ldg(pad_row + v);
+          else val[u] = Vec{};
+        } else if ((int32_t)i < L) {
+          val[u] = src[f];
+          dst_idx[u] = packed_idx;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dst_idx[u] >= 0) dst[dst_idx[u]] = val[u];
+  }
+}
+
+template <typename Vec>
+static ub_status launch_unpad_pad(bool pad, const void* src, void* dst, const int32_t* d_cu, const void* pad_row,
+                                  int32_t B, int32_t S, int64_t row_bytes, cudaStream_t s) {
+  const uint64_t V = row_bytes / sizeof(Vec);
+  const uint64_t n64 = (uint64_t)B * S * V;
+  UB_REQUIRE(n64 < (1ull << 32) - 1, UB_ERR_UNSUPPORTED, "padded tensor too large for one launch (%llu elems)",
+             (unsigned long long)n64);
+  const uint32_t n = (uint32_t)n64;
+  if (n == 0) return UB_OK;
+  const int threads = 256;
+  const uint64_t want = (n64 + threads * 4 - 1) / (threads * 4);
+  const int blocks = (int)(want < 148ull * 16 ? (want ? want : 1) : 148ull * 16);
+  FastDiv dv((uint32_t)V), ds((uint32_t)S);
+  if (pad)
+    unpad_pad_kernel<Vec, true><<<blocks, threads, 0, s>>>(static_cast<const Vec*>(src), static_cast<Vec*>(dst), d_cu,
+                                                          static_cast<const Vec*>(pad_row), n, dv, ds);
+  else
+    unpad_pad_kernel<Vec, false><<<blocks, threads, 0, s>>>(static_cast<const Vec*>(src), static_cast<Vec*>(dst), d_cu,
+                                                           nullptr, n, dv, ds);
+  UB_CHECK_LAUNCH();
+  return UB_OK;
+}
+
+static ub_status unpad_pad_dispatch(bool pad, const void* src, void* dst, const int32_t* d_cu, const void* pad_row,
+                                    int32_t B, int32_t S, int64_t T, int64_t row_bytes, void* stream) {
+  clear_error();
+  UB_REQUIRE(src && dst && d_cu, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(B >= 1 && S >= 1, UB_ERR_INVALID_ARG, "empty batch");
+  UB_REQUIRE(row_bytes > 0, UB_ERR_SHAPE, "row_bytes <= 0");
+  UB_REQUIRE(T >= 0 && T <= (int64_t)B * S, UB_ERR_CAPACITY, "T=%lld exceeds B*S", (long long)T);
+  const uintptr_t al = (uintptr_t)src | (uintptr_t)dst | (uintptr_t)(pad_row ? pad_row : dst);
+  cudaStream_t s = as_stream(stream);
+  if (row_bytes % 16 == 0 && (al & 15) == 0)
+    return launch_unpad_pad<int4>(pad, src, dst, d_cu, pad_row, B, S, row_bytes, s);
+  if (row_bytes % 4 == 0 && (al & 3) == 0)
+    return launch_unpad_pad<uint32_t>(pad, src, dst, d_cu, pad_row, B, S, row_bytes, s);
+  return launch_unpad_pad<uint8_t>(pad, src, dst, d_cu, pad_row, B, S, row_bytes, s);
+}
+
+// ------------------------------------------------------------------ exchange copy
+// One CTA per table entry: copies len*rec bytes of token records and srec bytes of the
+// sample record.  tab = {src_tok[B], len[B], dst_tok[B], src_smp[B], dst_smp[B]}.
+template <typename Vec>
+__global__ void __launch_bounds__(256) exchange_copy_kernel(const uint8_t* __restrict__ st, uint8_t* __restrict__ dt,
+                                                            const uint8_t* __restrict__ ss, uint8_t* __restrict__ ds,
+                                                            const int64_t* __restrict__ tab, int32_t B,
+                                                            int64_t rec, int64_t srec) {
+  const int e = blockIdx.x;
+  const int64_t src_tok = tab[e], len = tab[B + e], dst_tok = tab[2 * B + e];
+  const Vec* s = reinterpret_cast<const Vec*>(st + src_tok * rec);
+  Vec* d = reinterpret_cast<Vec*>(dt + dst_tok * rec);
+  const int64_t nv = len * rec / (int64_t)sizeof(Vec);
+  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d[i] = s[i];
+  if (srec > 0) {
+    const int64_t so = tab[3 * B + e] * srec, dso = tab[4 * B + e] * srec;
+    for (int64_t i = threadIdx.x; i < srec; i += blockDim.x) ds[dso + i] = ss[so + i];
+  }
+}
+
+}  // namespace ub
+
+using namespace ub;
+
+extern "C" ub_status ub_unpad(const void* padded, void* packed, const int32_t* d_cu, int32_t B, int32_t S,
+                              int64_t T, int64_t row_bytes, void* stream) {
+  return unpad_pad_dispatch(false, padded, packed, d_cu, nullptr, B, S, T, row_bytes, stream);
+}
+
+extern "C" ub_status ub_pad(const void* packed, void* padded, const int32_t* d_cu, int32_t B, int32_t S, int64_t T,
+                            int64_t row_bytes, const void* d_pad_row, void* stream) {
+  return unpad_pad_dispatch(true, packed, padded, d_cu, d_pad_row, B, S, T, row_bytes, stream);
+}
+
+extern "C" ub_status ub_exchange_copy(const void* src_tokens, void* dst_tokens, const void* src_samples,
+                                      void* dst_samples, const int64_t* d_tab, int32_t B, int64_t rec_bytes,
+                                      int64_t srec_bytes, void* stream) {
+  clear_error();
+  UB_REQUIRE(src_tokens && dst_tokens && d_tab, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(B >= 1 && rec_bytes > 0 && srec_bytes >= 0, UB_ERR_SHAPE, "bad sizes");
+  UB_REQUIRE(srec_bytes == 0 || (src_samples && dst_samples), UB_ERR_INVALID_ARG, "null sample pointer");
+  cudaStream_t s = as_stream(stream);
+  const uintptr_t al = (uintptr_t)src_tokens | (uintptr_t)dst_tokens;
+  auto* st = static_cast<const uint8_t*>(src_tokens);
+  auto* dt = static_cast<uint8_t*>(dst_tokens);
+  auto* ss = static_cast<const uint8_t*>(src_samples);
+  auto* ds = static_cast<uint8_t*>(dst_samples);
+  if (rec_bytes % 16 == 0 && (al & 15) == 0)
+    exchange_copy_kernel<int4><<<B, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
+  else if (rec_bytes % 4 == 0 && (al & 3) == 0)
+    exchange_copy_kernel<uint32_t><<<B, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
+  else
+    exchange_copy_kernel<uint8_t><<<B, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
+  UB_CHECK_LAUNCH();
+  return UB_OK;
+}

@@ -1,0 +1,139 @@
+"""Parity of the CUDA varlen FMHA (through the C ABI) against the fp64 oracle.  -m gpu."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from gpu_util import assert_close, errors, make_batch, oracle_seq_slice, TOL_LSE
+from oracle import attention as oatt
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ub():
+    import paper_2208_08124_b200 as ub
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    return ub
+
+
+def _run(ub, lengths, H, D, dtype, p=0.0, seed=7, max_seqlen=None, bwd=True):
+    lengths, off, qkv, dout = make_batch(lengths, H, D, dtype)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    ms = int(max_seqlen or lengths.max())
+    scale = 1.0 / math.sqrt(D)
+    qd, gd = qkv.cuda(), dout.cuda()
+    o, lse = ub.varlen_fmha_fwd(qd, cu, ms, scale, p, seed, 0)
+    d = ub.varlen_fmha_bwd(qd, o, lse, gd, cu, ms, scale, p, seed, 0) if bwd else None
+    torch.cuda.synchronize()
+    return lengths, off, qkv, dout, o.cpu(), lse.cpu(), (d.cpu() if d is not None else None), scale
+
+
+# BASELINE config 1: 4 sequences {3,7,1,5}, 2 heads x 8, fp32, vs CPU fp64 padded-masked attention
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_config1_tiny_fp32(ub, p):
+    lengths, off, qkv, dout, o, lse, d, scale = _run(ub, [3, 7, 1, 5], 2, 8, torch.float32, p=p)
+    q64, g64 = qkv.double().numpy(), dout.double().numpy()
+    O, LSE = oatt.varlen_fwd(q64, off, 7, scale, p, 7, 0)
+    dq = oatt.varlen_bwd(q64, g64, off, 7, scale, p, 7, 0)
+    assert_close(o.numpy(), O, "O", 1e-5, 1e-5)
+    assert_close(lse.numpy(), LSE, "LSE", 1e-5, 1e-5)
+    assert_close(d.numpy(), dq, "dqkv", 1e-4, 1e-5)
+
+
+EDGE_LENGTHS = [1, 127, 128, 129, 255, 256, 300, 512, 64, 2, 383, 384, 385]
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_bf16_edge_lengths_fwd_bwd(ub, p):
+    lengths, off, qkv, dout, o, lse, d, scale = _run(ub, EDGE_LENGTHS, 2, 64, torch.bfloat16, p=p, max_seqlen=512)
+    q64, g64 = qkv.double().numpy(), dout.double().numpy()
+    O, LSE = oatt.varlen_fwd(q64, off, 512, scale, p, 7, 0)
+    assert_close(o.float().numpy(), O, "O")
+    assert_close(lse.numpy(), LSE, "LSE", TOL_LSE, 1.0)
+    dq = oatt.varlen_bwd(q64, g64, off, 512, scale, p, 7, 0)
+    for i, name in enumerate("qkv"):
+        assert_close(d[:, i].float().numpy(), dq[:, i], "d" + name)
+
+
+def test_bf16_fwd_deterministic_and_single_sequence(ub):
+    lengths, off, qkv, dout = make_batch([200, 77], 3, 64)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    qd = qkv.cuda()
+    o1, l1 = ub.varlen_fmha_fwd(qd, cu, 512)
+    o2, l2 = ub.varlen_fmha_fwd(qd, cu, 512)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    # L = 1: output equals the V row exactly up to bf16 rounding
+    lengths, off, qkv, dout = make_batch([1, 1, 1], 2, 64)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    o, lse = ub.varlen_fmha_fwd(qkv.cuda(), cu, 512)
+    torch.cuda.synchronize()
+    assert torch.equal(o.cpu(), qkv[:, 2])
+    d = ub.varlen_fmha_bwd(qkv.cuda(), o, lse, dout.cuda(), cu, 512)
+    torch.cuda.synchronize()
+    d = d.cpu().float()
+    assert torch.all(d[:, 0] == 0) and torch.all(d[:, 1] == 0)       # L=1: dQ = dK = 0
+    assert torch.equal(d[:, 2], dout.float())                         # dV = dO
+
+
+@pytest.mark.parametrize("dist,seed", [("mlperf_like_v0", 0), ("uniform", 1), ("bimodal", 2)])
+def test_bf16_bert_large_full_size_sampled(ub, dist, seed):
+    """BASELINE config 2 / 5 at full size (56 x up to 512, 16 heads x 64) in the launch
+    configuration bench.py times; the oracle checks a sample of sequences one by one
+    (longest, shortest and a few in between), plus size-independent invariants."""
+    L = synth.gen_lengths(dist, 56, seed)
+    lengths, off, qkv, dout, o, lse, d, scale = _run(ub, L, 16, 64, torch.bfloat16, p=0.0, max_seqlen=512)
+    order = np.argsort(L)
+    seqs = sorted(set([int(order[0]), int(order[-1]), int(order[len(order) // 2]), int(order[len(order) // 4]),
+                       int(order[3 * len(order) // 4])]))
+    ref = oracle_seq_slice(qkv, dout, off, seqs, scale)
+    for b in seqs:
+        s, e = int(off[b]), int(off[b + 1])
+        O, LSE, dq = ref[b]
+        assert_close(o[s:e].float().numpy(), O, f"O seq{b}")
+        assert_close(lse[:, s:e].numpy(), LSE, f"LSE seq{b}", TOL_LSE, 1.0)
+        for i, name in enumerate("qkv"):
+            assert_close(d[s:e, i].float().numpy(), dq[:, i], f"d{name} seq{b}")
+    # invariants at full size: sum_j dK_j = 0 and sum_j dV_j = sum_i dO_i per (seq, head)
+    d32, g32 = d.float(), dout.float()
+    for b in range(len(L)):
+        s, e = int(off[b]), int(off[b + 1])
+        dk_sum = d32[s:e, 1].sum(0)
+        assert float(dk_sum.abs().max()) < 0.05 * max(1.0, math.sqrt(e - s)), b
+        assert_close(d32[s:e, 2].sum(0).numpy(), g32[s:e].sum(0).numpy(), f"sum dV seq{b}", 0.05 * math.sqrt(e - s), 2e-2)
+
+
+def test_bf16_dropout_mask_matches_oracle(ub):
+    """With V = identity-like one-hot rows, O exposes P~ directly: the GPU's dropout
+    pattern must equal the oracle's Philox mask (R5) bitwise (kept <=> nonzero)."""
+    L, H, D = 64, 2, 64
+    lengths, off, qkv, dout = make_batch([L], H, D)
+    qkv[:, 2] = 0
+    for j in range(L):
+        qkv[j, 2, :, j] = 1.0                       # v_j = e_j -> O[i, d=j] = P~[i, j]
+    qd = qkv.cuda()
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    o, _ = ub.varlen_fmha_fwd(qd, cu, 512, None, 0.3, 1234, 5)
+    torch.cuda.synchronize()
+    from oracle import philox
+    for h in range(H):
+        keep = philox.keep_mask_block(1234, 5, 0, L, h, 0.3)
+        got = (o[:, h, :L].float().cpu().numpy() != 0)
+        assert np.array_equal(got, keep), h
+
+
+def test_invalid_arguments(ub):
+    from paper_2208_08124_b200._lib import UbError
+    lengths, off, qkv, dout = make_batch([5], 2, 32)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    with pytest.raises(UbError) as e:
+        ub.varlen_fmha_fwd(qkv.cuda(), cu, 512)       # bf16 path supports head_dim 64 only
+    assert e.value.status == 5
+    lengths, off, qkv, dout = make_batch([5], 2, 64)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    with pytest.raises(UbError) as e:
+        ub.varlen_fmha_fwd(qkv.cuda(), cu, 512, p_dropout=1.0)
+    assert e.value.status == 1
