@@ -1,0 +1,508 @@
+#!/usr/bin/env python
+"""bench.py -- the unpadded-BERT hot path (arXiv 2208.08124) on B200, one JSON line.
+
+A step is one pass of every row of SURVEY.md §8(a) over one 56-sequence BERT-large batch
+per GPU (H=16, D=64, max_seqlen 512, MLPerf-like length mix, bf16):
+  side stream (prepared one step ahead):
+    a6 unpad   padded input records [56, 512, 16 B] -> packed [T, 16 B]
+    a1-a5      balance_exchange: NCCL all-gather of lengths, host plan (sort + interleave,
+               P:355-359), pack, grouped ncclSend/ncclRecv, reorder, cu_seqlens H2D
+  main stream:
+    a7 varlen FMHA forward over the exchanged cu_seqlens
+    a8 varlen FMHA backward (dO given)
+    a9 pad     attention output [T, 1024] -> [56, 512, 1024]
+Metric (BASELINE.json): unpadded FMHA fwd+bwd tokens/s, with the roofline fraction of the
+dominant kernel and the 8-GPU token imbalance.
+
+Usage: python bench.py --gpus N --steps K --warmup W [--impl reference]
+       (N > 1: torchrun --nproc-per-node N ... bench.py --gpus N ...)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+H, D, S, B = 16, 64, 512, 56
+REC = 16      # per-token record: input_id, segment_id, masked_lm_label, position (int32 x 4)
+SREC = 4      # per-sample record: next_sentence_label (int32)
+N_SETS = 3    # rotating input sets: each step's working set (> 300 MB) and the 2 others exceed L2
+KERNELS_PER_STEP = 10   # ours: unpad, 2x exchange copy, fwd plan+main, bwd plan+pre+main+dq, pad
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dist", default="mlperf_like_v0", choices=list(synth.DISTRIBUTIONS))
+    ap.add_argument("--p-dropout", type=float, default=0.0)
+    ap.add_argument("--balance", default="paper", choices=["paper", "snake"])
+    ap.add_argument("--skew", default="iid", choices=["iid", "sorted-block"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--reserve-sms", type=int, default=4)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sust": d.get("bf16_tflops_sustained"),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sust": 1400.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+def load_traffic():
+    """dram bytes per launch from the committed ncu --set full summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f).get("dram_bytes_per_launch", {})
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.path = index, None, None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [x for x in sm if x > 0.5 * (max(sm) if sm else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_init(n):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n:
+        raise SystemExit(f"--gpus {n} but WORLD_SIZE={world} (launch N>1 with torchrun)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _red_dev():
+    import torch.distributed as dist
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
+
+
+def all_max(x, world):
+    """Max over ranks (timing: the job is as slow as its slowest rank)."""
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=_red_dev())
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def all_sum(x, world):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=_red_dev())
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def all_gather_list(x, world):
+    if world == 1:
+        return [x]
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=_red_dev())
+    out = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    return [float(o.item()) for o in out]
+
+
+def rank_lengths(args, world, rank, s):
+    return synth.skewed_rank_lengths(world, B, s, args.skew, args.dist)[rank]
+
+
+def flops_fwd(L):
+    return 4.0 * H * D * float(np.sum(np.asarray(L, np.float64) ** 2))
+
+
+def flops_bwd(L):
+    return 8.0 * H * D * float(np.sum(np.asarray(L, np.float64) ** 2))
+
+
+# ------------------------------------------------------------------ oracle legs
+def oracle_sample(qkv_cpu, dout_cpu, L, seqs, scale):
+    """fwd + bwd of the fp64 oracle on the listed sequences; returns tokens processed."""
+    from oracle import attention as oatt
+    from oracle import varlen as ovar
+    off = ovar.batch_offset(L)
+    q64 = qkv_cpu.double().numpy()
+    g64 = dout_cpu.double().numpy()
+    tok = 0
+    for b in seqs:
+        s, e = int(off[b]), int(off[b + 1])
+        sub = np.array([0, e - s])
+        oatt.varlen_fwd(q64[s:e], sub, e - s, scale)
+        oatt.varlen_bwd(q64[s:e], g64[s:e], sub, e - s, scale)
+        tok += e - s
+    return tok
+
+
+def cpu_baseline(args, seconds):
+    """The oracle as it stands, timed on this host's cores on a bounded sample of the
+    workload (sequences of batch 0 in order, fwd+bwd, until `seconds` elapse)."""
+    L = synth.gen_lengths(args.dist, B, 100)
+    T = int(L.sum())
+    qkv = synth.gen_normal((T, 3, H, D), 1000)
+    dout = synth.gen_normal((T, H, D), 2000)
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    tok, n = 0, 0
+    while n < B and time.perf_counter() - t0 < seconds:
+        tok += oracle_sample(qkv, dout, L, [n], 1 / math.sqrt(D))
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": tok / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"fp64 numpy oracle fwd+bwd on the first {n} of 56 sequences ({tok} tokens) of one "
+                      f"{args.dist} batch, H=16 D=64, {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle is this tier's reference arm (rank 0 only)."""
+    if rank != 0:
+        return None
+    L = synth.gen_lengths(args.dist, B, 100)
+    T = int(L.sum())
+    qkv = synth.gen_normal((T, 3, H, D), 1000)
+    dout = synth.gen_normal((T, H, D), 2000)
+    order = list(np.argsort(L))
+    per_step = 2
+    for w in range(args.warmup):
+        oracle_sample(qkv, dout, L, [order[(2 * w) % B]], 1 / math.sqrt(D))
+    t0 = time.perf_counter()
+    tok = 0
+    for k in range(args.steps):
+        seqs = [int(order[(k * per_step + j * 17) % B]) for j in range(per_step)]
+        tok += oracle_sample(qkv, dout, L, seqs, 1 / math.sqrt(D))
+    dt = time.perf_counter() - t0
+    v = tok / dt
+    cores = len(os.sched_getaffinity(0))
+    return {"metric": "unpadded FMHA fwd+bwd tokens/s (BERT-large)", "impl": "reference", "value": v,
+            "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"bert_large_fmha_{args.dist}", "batch_per_gpu": B, "heads": H, "head_dim": D,
+                       "max_seqlen": S},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} sequences per step of one {args.dist} batch, fwd+bwd fp64"},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ------------------------------------------------------------------ our arm
+class Workload:
+    def __init__(self, args, world, rank, dev):
+        import paper_2208_08124_b200 as ub
+        self.ub, self.args, self.world, self.rank, self.dev = ub, args, world, rank, dev
+        self.cap = B * S
+        self.sets = []
+        for s in range(N_SETS):
+            L = rank_lengths(args, world, rank, s)
+            recs = np.zeros((B, S, 4), np.int32)
+            raw = synth.gen_bytes(B * S * 16, 500 + 10 * s + rank).view(np.int32).reshape(B, S, 4) & 0x7FFF
+            for b in range(B):
+                recs[b, :L[b]] = raw[b, :L[b]]
+            smp = synth.gen_bytes(B * 4, 600 + s + rank).view(np.int32).reshape(B, 1) & 1
+            off = ub.cu_seqlens(L, S)
+            st = {"L": L, "T": int(off[-1]), "lengths": torch.from_numpy(L).to(dev),
+                  "cu_local": torch.from_numpy(off).to(dev), "padded_recs": torch.from_numpy(recs).to(dev),
+                  "samples": torch.from_numpy(smp).to(dev),
+                  "qkv": synth.gen_normal_device((self.cap, 3, H, D), 1000 + 7 * s + 100 * rank, dev),
+                  "dout": synth.gen_normal_device((self.cap, H, D), 2000 + 7 * s + 100 * rank, dev)}
+            self.sets.append(st)
+        self.packed_recs = torch.empty((self.cap, 4), dtype=torch.int32, device=dev)
+        self.ex = [{"tokens": torch.empty((self.cap, 4), dtype=torch.int32, device=dev),
+                    "samples": torch.empty((B, 1), dtype=torch.int32, device=dev),
+                    "cu": torch.empty(B + 1, dtype=torch.int32, device=dev), "T": 0, "L": None} for _ in range(2)]
+        self.out = torch.empty((self.cap, H, D), dtype=torch.bfloat16, device=dev)
+        self.lse = torch.empty((H, self.cap), dtype=torch.float32, device=dev)
+        self.dqkv = torch.empty((self.cap, 3, H, D), dtype=torch.bfloat16, device=dev)
+        self.padded_out = torch.empty((B, S, H, D), dtype=torch.bfloat16, device=dev)
+        self.main = torch.cuda.current_stream()
+        self.side = torch.cuda.Stream()
+        self.ex_ready = [torch.cuda.Event() for _ in range(2)]
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        self.comm = ub.Comm(world, rank)
+        # leave SMs free for the side-stream exchange (NCCL + copy kernels) to run
+        # concurrently with the persistent FMHA kernels (P:376-381 overlap)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.ctas = sms - args.reserve_sms
+
+    def prepare(self, n):
+        """Side stream, one step ahead: a6 unpad of step n's input records, a1-a5 exchange."""
+        st, ex = self.sets[n % N_SETS], self.ex[n % 2]
+        self.side.wait_event(self.done[n % 2])            # step n-2 finished with these buffers
+        with torch.cuda.stream(self.side):
+            self.ub.unpad(st["padded_recs"], st["cu_local"], st["T"], out=self.packed_recs[:st["T"]],
+                          stream=self.side)
+            _, _, _, T, perm = self.comm.balance_exchange(
+                st["lengths"], self.packed_recs[:st["T"]], st["samples"], self.cap, S, self.args.balance,
+                out_tokens=ex["tokens"], out_samples=ex["samples"], out_cu=ex["cu"], stream=self.side)
+        allL = np.asarray(self.all_lengths_cache(n), np.int64)
+        ex["T"] = T
+        ex["L"] = allL[perm[self.rank * B:(self.rank + 1) * B]]
+        self.ex_ready[n % 2].record(self.side)
+
+    def all_lengths_cache(self, n):
+        s = n % N_SETS
+        return synth.skewed_rank_lengths(self.world, B, s, self.args.skew, self.args.dist).reshape(-1)
+
+    def step(self, n, prof=None):
+        """Main stream: a7 fwd, a8 bwd, a9 pad for step n."""
+        st, ex = self.sets[n % N_SETS], self.ex[n % 2]
+        T = ex["T"]
+        self.main.wait_event(self.ex_ready[n % 2])
+        p = self.args.p_dropout
+        if prof is not None:
+            for kid, pair in prof.items():
+                self.ub.api.profile_events(kid, *pair)
+        self.ub.varlen_fmha_fwd(st["qkv"][:T], ex["cu"], S, None, p, 0x2208 + n, 0, out=self.out[:T],
+                                lse=self.lse, num_ctas=self.ctas)
+        self.ub.varlen_fmha_bwd(st["qkv"][:T], self.out[:T], self.lse, st["dout"][:T], ex["cu"], S, None, p,
+                                0x2208 + n, 0, dqkv=self.dqkv[:T], num_ctas=self.ctas)
+        self.ub.pad(self.out[:T], ex["cu"], B, S, out=self.padded_out)
+        self.done[n % 2].record(self.main)
+        return T
+
+
+def run_ours(args, world, rank, local):
+    dev = torch.device("cuda", local)
+    wl = Workload(args, world, rank, dev)
+    ub = wl.ub
+    peaks = load_peaks()
+    # warm-up
+    wl.prepare(0)
+    for n in range(args.warmup):
+        _patch_lse(wl, n)
+        wl.step(n)
+        wl.prepare(n + 1)
+    torch.cuda.synchronize()
+    barrier(world)
+    # timed region
+    kids = [ub.api.PROF_FWD, ub.api.PROF_BWD, ub.api.PROF_PAD, ub.api.PROF_UNPAD]
+    prof_events = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in kids}
+                   for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tokens, lens_used = 0, []
+    e0.record(wl.main)
+    for k in range(args.steps):
+        n = args.warmup + k
+        _patch_lse(wl, n)
+        tokens += wl.step(n, prof_events[k])
+        lens_used.append(wl.ex[n % 2]["L"])
+        wl.prepare(n + 1)
+    wl.main.wait_event(wl.ex_ready[(args.warmup + args.steps) % 2])
+    e1.record(wl.main)
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    for kid in kids:
+        ub.api.profile_events(kid)
+    ms = e0.elapsed_time(e1)
+    ms_max = all_max(ms, world)
+    tok_all = all_sum(tokens, world)
+    value = tok_all / (ms_max / 1e3)
+    per_rank_tokens = all_gather_list(tokens / args.steps, world)
+    imbalance = max(per_rank_tokens) / (sum(per_rank_tokens) / world) - 1.0
+
+    # per-kernel device time (events on the launching stream)
+    kt = {k: [prof_events[i][k][0].elapsed_time(prof_events[i][k][1]) for i in range(args.steps)] for k in kids}
+    f_fwd = [flops_fwd(L) for L in lens_used]
+    f_bwd = [flops_bwd(L) for L in lens_used]
+    fwd_us, bwd_us = np.mean(kt[kids[0]]) * 1e3, np.mean(kt[kids[1]]) * 1e3
+    pad_us, unpad_us = np.mean(kt[kids[2]]) * 1e3, np.mean(kt[kids[3]]) * 1e3
+    fwd_tf = np.mean(f_fwd) / (fwd_us * 1e-6) / 1e12
+    bwd_tf = np.mean(f_bwd) / (bwd_us * 1e-6) / 1e12
+    mean_T = tokens / args.steps
+    pad_bytes = mean_T * H * D * 2 + B * S * H * D * 2
+    pad_gbs = pad_bytes / (pad_us * 1e-6) / 1e9
+    peak_tc = peaks["bf16_sust"] or peaks["bf16"]
+    dom = "bwd" if bwd_us >= fwd_us else "fwd"
+    achieved = bwd_tf if dom == "bwd" else fwd_tf
+    traffic = load_traffic().get("fmha_" + dom)
+    roofline = {"kernel": f"fmha_{dom}_kernel", "bound": "tensor", "achieved": round(achieved, 2),
+                "peak": peak_tc, "unit": "TFLOP/s", "frac": round(achieved / peak_tc, 4), "traffic": traffic,
+                "peak_source": peaks["src"] + " bf16_tflops_sustained (kernel timed inside a long step loop)",
+                "flops_convention": "algorithmic, no recompute credit: fwd 4*H*D*sum(L^2), bwd 8*H*D*sum(L^2)",
+                "frac_of_burst_peak": round(achieved / peaks["bf16"], 4)}
+    kernels = {"fmha_fwd": {"us": round(fwd_us, 2), "tflops": round(fwd_tf, 1)},
+               "fmha_bwd": {"us": round(bwd_us, 2), "tflops": round(bwd_tf, 1)},
+               "pad": {"us": round(pad_us, 2), "GBps": round(pad_gbs, 1), "frac_hbm": round(pad_gbs / peaks["hbm"], 3)},
+               "unpad_records": {"us": round(unpad_us, 2)}}
+    fmha_only = mean_T * world / ((fwd_us + bwd_us) * 1e-6)
+
+    e2e = None if args.no_e2e else run_e2e(args, wl, world)
+    out = {"metric": "unpadded FMHA fwd+bwd tokens/s (BERT-large)", "value": round(value, 1), "unit": "tokens/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (seeded lengths + N(0,1) bf16 qkv/dO; no dataset)",
+           "config": {"workload": f"bert_large_fmha_{args.dist}", "batch_per_gpu": B, "heads": H, "head_dim": D,
+                      "max_seqlen": S, "p_dropout": args.p_dropout, "balance": args.balance, "skew": args.skew,
+                      "parallelism": f"dp{world}", "fmha_ctas": wl.ctas, "l2": "rotating 3 input sets; per-step working set > L2",
+                      "step": "unpad records + exchange (side stream) | fmha fwd + bwd + pad (main stream)"},
+           "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
+           "imbalance": round(imbalance, 5), "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk}
+    if e2e is not None:
+        out["e2e"] = e2e
+    return out, wl
+
+
+def _patch_lse(wl, n):
+    """The ABI wants lse as a dense [H, T] array: view the front of the buffer per step."""
+    T = wl.ex[n % 2]["T"]
+    if not hasattr(wl, "lse_full"):
+        wl.lse_full = wl.lse
+    wl.lse = wl.lse_full.view(-1)[:H * max(T, 1)].view(H, max(T, 1))
+
+
+def run_e2e(args, wl, world):
+    """Same step through the public API with HOST inputs: per step the padded input
+    records, lengths, sample records, qkv and dO are copied H2D from pinned memory and the
+    step's result (dqkv) is read back D2H, all inside the timed region."""
+    host = []
+    for s in range(N_SETS):
+        st = wl.sets[s]
+        T = st["T"]
+        host.append({"recs": st["padded_recs"].cpu().pin_memory(), "lengths": st["lengths"].cpu().pin_memory(),
+                     "samples": st["samples"].cpu().pin_memory(),
+                     "qkv": st["qkv"][:wl.cap].cpu().pin_memory(), "dout": st["dout"].cpu().pin_memory()})
+    dq_host = torch.empty((wl.cap, 3, H, D), dtype=torch.bfloat16).pin_memory()
+    h2d = d2h = 0
+
+    def one(n):
+        nonlocal h2d, d2h
+        s = n % N_SETS
+        st, hs = wl.sets[s], host[s]
+        with torch.cuda.stream(wl.side):
+            st["padded_recs"].copy_(hs["recs"], non_blocking=True)
+            st["lengths"].copy_(hs["lengths"], non_blocking=True)
+            st["samples"].copy_(hs["samples"], non_blocking=True)
+        wl.prepare(n)
+        T = wl.ex[n % 2]["T"]
+        st["qkv"][:T].copy_(hs["qkv"][:T], non_blocking=True)
+        st["dout"][:T].copy_(hs["dout"][:T], non_blocking=True)
+        _patch_lse(wl, n)
+        wl.step(n)
+        dq_host[:T].copy_(wl.dqkv[:T], non_blocking=True)
+        h2d += hs["recs"].numel() * 4 + B * 4 + B * 4 + T * 3 * H * D * 2 + T * H * D * 2
+        d2h += T * 3 * H * D * 2
+        return T
+
+    base = 10 ** 6
+    for n in range(min(args.warmup, 3)):
+        one(base + n)
+    torch.cuda.synchronize()
+    barrier(world)
+    h2d = d2h = 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(wl.main)
+    tok = 0
+    for k in range(args.steps):
+        tok += one(base + 10 + k)
+    e1.record(wl.main)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = all_max(e0.elapsed_time(e1), world)
+    tok_all = all_sum(tok, world)
+    return {"value": round(tok_all / (ms / 1e3), 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d // args.steps),
+            "d2h_bytes_per_step": int(d2h // args.steps)}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    world, rank, local = dist_init(args.gpus)
+    out, wl = run_ours(args, world, rank, local)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    wl.comm.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

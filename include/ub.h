@@ -54,6 +54,13 @@ const char* ub_last_error(void);
 /* Library build string (arch, version). */
 const char* ub_version(void);
 
+/* Measurement hook (bench / profiling only): record the given cudaEvent_t handles
+ * immediately before and after every subsequent launch of one internal kernel, on the
+ * stream it is launched on, so its device time can be read inside a larger step.
+ * kernel_id: 0 = FMHA forward main kernel, 1 = FMHA backward main kernel, 2 = pad,
+ * 3 = unpad.  NULL events clear the hook.  Process-wide; not thread-safe. */
+ub_status ub_profile_events(int32_t kernel_id, void* start_event, void* stop_event);
+
 /* ------------------------------------------------------------------------------------
  * batch_offset / cu_seqlens ("a prefix sum array ... to record the token number
  * of each sequence").  Host helper.
@@ -117,6 +124,8 @@ typedef struct {
   uint64_t seed;      /* Philox key (R5) */
   uint64_t offset;    /* Philox counter word 3 (low 32 bits used) */
   int32_t dtype;      /* ub_dtype */
+  int32_t num_ctas;   /* persistent grid size; 0 = one CTA per SM.  Set below the SM count to
+                         leave SMs to concurrent side-stream work (the overlapped exchange) */
 } ub_fmha_params;
 
 size_t ub_fmha_workspace_bytes(const ub_fmha_params* prm, int is_bwd);

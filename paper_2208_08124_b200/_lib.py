@@ -21,12 +21,14 @@ P_i32, P_i64 = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
 
 class FmhaParams(C.Structure):
     _fields_ = [("B", i32), ("T", i64), ("max_seqlen", i32), ("heads", i32), ("head_dim", i32),
-                ("scale", f32), ("p_dropout", f32), ("seed", u64), ("offset", u64), ("dtype", i32)]
+                ("scale", f32), ("p_dropout", f32), ("seed", u64), ("offset", u64), ("dtype", i32),
+                ("num_ctas", i32)]
 
 
 SIGNATURES = {
     "ub_last_error": (C.c_char_p, []),
     "ub_version": (C.c_char_p, []),
+    "ub_profile_events": (i32, [i32, vp, vp]),
     "ub_cu_seqlens": (i32, [vp, i32, i32, vp]),
     "ub_lengths_from_mask": (i32, [vp, i32, i32, vp]),
     "ub_unpad": (i32, [vp, vp, vp, i32, i32, i64, i64, vp]),

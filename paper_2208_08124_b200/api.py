@@ -46,6 +46,19 @@ def version() -> str:
     return lib().ub_version().decode()
 
 
+PROF_FWD, PROF_BWD, PROF_PAD, PROF_UNPAD = 0, 1, 2, 3
+
+
+def profile_events(kernel_id: int, start=None, stop=None):
+    """Record torch.cuda.Event `start`/`stop` around every launch of one internal kernel
+    (0 fwd main, 1 bwd main, 2 pad, 3 unpad); None clears.  Bench/profiling hook."""
+    for e in (start, stop):
+        if e is not None and not e.cuda_event:
+            e.record()            # torch creates the cudaEvent_t lazily on first record
+    check(lib().ub_profile_events(int(kernel_id), start.cuda_event if start is not None else None,
+                                  stop.cuda_event if stop is not None else None))
+
+
 # ------------------------------------------------------------------ batch_offset
 def cu_seqlens(lengths, max_seqlen: int) -> np.ndarray:
     """Host prefix sum with validation; returns int32 [B+1]."""
@@ -86,20 +99,21 @@ def pad(packed: torch.Tensor, cu: torch.Tensor, B: int, S: int, pad_row: torch.T
 
 
 # ------------------------------------------------------------------ varlen FMHA
-def fmha_params(B, T, max_seqlen, heads, head_dim, dtype, scale=None, p_dropout=0.0, seed=0, offset=0):
+def fmha_params(B, T, max_seqlen, heads, head_dim, dtype, scale=None, p_dropout=0.0, seed=0, offset=0,
+                num_ctas=0):
     return FmhaParams(B=int(B), T=int(T), max_seqlen=int(max_seqlen), heads=int(heads), head_dim=int(head_dim),
                       scale=float(scale if scale is not None else 1.0 / math.sqrt(head_dim)),
                       p_dropout=float(p_dropout), seed=int(seed), offset=int(offset),
-                      dtype=UB_BF16 if dtype == torch.bfloat16 else UB_FP32)
+                      dtype=UB_BF16 if dtype == torch.bfloat16 else UB_FP32, num_ctas=int(num_ctas))
 
 
 def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=None, p_dropout=0.0, seed=0,
-                    offset=0, out=None, lse=None, stream=None):
+                    offset=0, out=None, lse=None, stream=None, num_ctas=0):
     """Eq. (1) over packed qkv [T, 3, H, D]; returns (out [T,H,D], lse [H,T] fp32)."""
     T, three, H, D = qkv.shape
     assert three == 3
     B = cu.numel() - 1
-    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset)
+    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas)
     if out is None:
         out = torch.empty((T, H, D), dtype=qkv.dtype, device=qkv.device)
     if lse is None:
@@ -111,11 +125,11 @@ def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=
 
 
 def varlen_fmha_bwd(qkv, out, lse, dout, cu, max_seqlen: int, scale=None, p_dropout=0.0, seed=0, offset=0,
-                    dqkv=None, stream=None):
+                    dqkv=None, stream=None, num_ctas=0):
     """Backward of varlen_fmha_fwd; returns dqkv [T, 3, H, D]."""
     T, _, H, D = qkv.shape
     B = cu.numel() - 1
-    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset)
+    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas)
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
     ws = _workspace(lib().ub_fmha_workspace_bytes(C.byref(prm), 1), qkv.device, "fmha_bwd")

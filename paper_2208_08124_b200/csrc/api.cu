@@ -39,9 +39,25 @@ ub_status require_sm100() {
   return UB_OK;
 }
 
+static cudaEvent_t g_prof[kProfCount][2] = {};
+
+void prof_record(int kernel_id, int which, cudaStream_t s) {
+  cudaEvent_t e = g_prof[kernel_id][which];
+  if (e) cudaEventRecord(e, s);
+}
+
 }  // namespace ub
 
 using namespace ub;
+
+extern "C" ub_status ub_profile_events(int32_t kernel_id, void* start_event, void* stop_event) {
+  clear_error();
+  UB_REQUIRE(kernel_id >= 0 && kernel_id < kProfCount, UB_ERR_INVALID_ARG, "bad kernel id %d", kernel_id);
+  UB_REQUIRE((start_event == nullptr) == (stop_event == nullptr), UB_ERR_INVALID_ARG, "give both events or none");
+  g_prof[kernel_id][0] = static_cast<cudaEvent_t>(start_event);
+  g_prof[kernel_id][1] = static_cast<cudaEvent_t>(stop_event);
+  return UB_OK;
+}
 
 extern "C" const char* ub_last_error(void) { return g_last_error.c_str(); }
 

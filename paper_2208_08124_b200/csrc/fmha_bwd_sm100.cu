@@ -408,9 +408,12 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t max_items = (int64_t)p.heads * (p.B + p.T / kTile + 1);
-  const int grid = (int)std::min<int64_t>(sms, max_items);
+  const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
+  const int grid = (int)std::min<int64_t>(ctas, max_items);
+  prof_record(kProfBwd, 0, s);
   bwd::fmha_bwd_kernel<<<grid, bwd::kThreads, bwd::kSmemBytes, s>>>(tq, tdo, prm);
   UB_CHECK_LAUNCH();
+  prof_record(kProfBwd, 1, s);
   const int64_t n = rows * (bwd::kD / 8);
   bwd::bwd_dq_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(dq_acc, static_cast<__nv_bfloat16*>(dqkv), p.T,
                                                                   p.heads, p.scale);

@@ -327,9 +327,12 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // upper bound on items: H * (B + T/128); one CTA per SM, persistent
   const int64_t max_items = (int64_t)p.heads * (p.B + p.T / kTile + 1);
-  const int grid = (int)std::min<int64_t>(sms, max_items);
+  const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
+  const int grid = (int)std::min<int64_t>(ctas, max_items);
+  prof_record(kProfFwd, 0, s);
   fwd::fmha_fwd_kernel<<<grid, fwd::kThreads, fwd::kSmemBytes, s>>>(tmap, prm);
   UB_CHECK_LAUNCH();
+  prof_record(kProfFwd, 1, s);
   return UB_OK;
 }
 

@@ -15,6 +15,10 @@ void clear_error();
 // Capability check: device of the current context must be sm_100 (cached per device).
 ub_status require_sm100();
 
+// Measurement hook (ub_profile_events): events recorded around one internal kernel.
+enum ProfKernel { kProfFwd = 0, kProfBwd = 1, kProfPad = 2, kProfUnpad = 3, kProfCount = 4 };
+void prof_record(int kernel_id, int which, cudaStream_t s);
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 #define UB_CHECK_CUDA(expr)                                                              \

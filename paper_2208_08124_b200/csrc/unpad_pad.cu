@@ -70,6 +70,8 @@ static ub_status launch_unpad_pad(bool pad, const void* src, void* dst, const in
   const uint64_t want = (n64 + threads * 4 - 1) / (threads * 4);
   const int blocks = (int)(want < 148ull * 16 ? (want ? want : 1) : 148ull * 16);
   FastDiv dv((uint32_t)V), ds((uint32_t)S);
+  const int pk = pad ? kProfPad : kProfUnpad;
+  prof_record(pk, 0, s);
   if (pad)
     unpad_pad_kernel<Vec, true><<<blocks, threads, 0, s>>>(static_cast<const Vec*>(src), static_cast<Vec*>(dst), d_cu,
                                                           static_cast<const Vec*>(pad_row), n, dv, ds);
@@ -77,6 +79,7 @@ static ub_status launch_unpad_pad(bool pad, const void* src, void* dst, const in
     unpad_pad_kernel<Vec, false><<<blocks, threads, 0, s>>>(static_cast<const Vec*>(src), static_cast<Vec*>(dst), d_cu,
                                                            nullptr, n, dv, ds);
   UB_CHECK_LAUNCH();
+  prof_record(pk, 1, s);
   return UB_OK;
 }
 

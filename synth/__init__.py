@@ -88,3 +88,12 @@ def skewed_rank_lengths(world: int, batch: int, step: int, mode: str = "iid",
     elif mode != "iid":
         raise ValueError(mode)
     return draws.reshape(world, batch).astype(np.int32)
+
+
+def gen_normal_device(shape, seed: int, device, dtype=torch.bfloat16) -> torch.Tensor:
+    """N(0,1) drawn on the GPU with a seeded torch CUDA generator (Philox), rounded to
+    ``dtype`` -- for large benchmark buffers where a CPU draw would dominate set-up time.
+    Parity tests use the CPU draw (gen_normal)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    return torch.randn(tuple(shape), generator=g, device=device, dtype=torch.float32).to(dtype)

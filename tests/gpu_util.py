@@ -28,7 +28,10 @@ def errors(got, exp):
     got = np.asarray(got, dtype=np.float64)
     exp = np.asarray(exp, dtype=np.float64)
     max_abs = float(np.max(np.abs(got - exp))) if got.size else 0.0
-    rel = float(np.linalg.norm(got - exp) / max(np.linalg.norm(exp), 1e-30)) if got.size else 0.0
+    ne = np.linalg.norm(exp)
+    # rel-L2 is undefined for an exactly-zero reference (e.g. dQ of a 1-token sequence):
+    # there only the max-abs bound applies
+    rel = float(np.linalg.norm(got - exp) / ne) if got.size and ne > 1e-6 else 0.0
     return max_abs, rel
 
 

@@ -75,7 +75,8 @@ def test_bf16_fwd_deterministic_and_single_sequence(ub):
     d = ub.varlen_fmha_bwd(qkv.cuda(), o, lse, dout.cuda(), cu, 512)
     torch.cuda.synchronize()
     d = d.cpu().float()
-    assert torch.all(d[:, 0] == 0) and torch.all(d[:, 1] == 0)       # L=1: dQ = dK = 0
+    # L=1: dQ = dK = 0 (dS = P (dP - Delta) with P = 1 and dP = Delta up to fp32 summation order)
+    assert float(d[:, 0].abs().max()) < 1e-5 and float(d[:, 1].abs().max()) < 1e-5
     assert torch.equal(d[:, 2], dout.float())                         # dV = dO
 
 
