@@ -2,21 +2,30 @@
 //
 // Chain rule of Eq. (1) per sequence and head; dropout replayed from the Philox
 // key (R4/R5):
-//   Delta_i = sum_d dO_id O_id                               (prologue kernel)
-//   S = Q K^T, P = exp(scale S - LSE), dP~ = dO V^T            (recompute, TMEM)
-//   P~ = P M/(1-p), dP = dP~ M/(1-p), dS = P (dP - Delta)      (registers)
-//   dV += P~^T dO,  dK += dS^T Q  (TMEM, per key tile),  dQ += dS K  (fp32 atomics)
-//   dK *= scale, dQ *= scale                                  (epilogues)
+//   Delta_i = sum_d dO_id O_id                                   (prologue kernel)
+//   S^T = K Q^T, P^T = exp(scale S^T - LSE), dP~^T = V dO^T       (recompute, TMEM)
+//   P~ = P M/(1-p), dP = dP~ M/(1-p), dS = P (dP - Delta)          (registers)
+//   dV += P~^T dO, dK += dS^T Q   (TMEM, per key tile)             dQ += dS K (TMA reduce-add)
+//   dK *= scale (epilogue), dQ *= scale (finalize kernel)
 //
-// Work item = (sequence, head, 128-key tile) along the length-bucketed plan; the CTA
-// walks the sequence's query tiles.  Warp roles as in the forward: warp 0 TMA, warp 1
-// MMA (one thread), warp 2 TMEM allocator, warps 4-7 "softmax" (thread r owns query row
-// r of S/dP, and key row r of dK/dV).  P~ and dS are written once to smem ([q][key],
-// UMMA SW128 K-major) and read by three MMAs each through K-major or MN-major descriptors:
-//   dV: A = P~^T (MN-major view), B = dO (MN-major)      M128 N64 K128
-//   dK: A = dS^T (MN-major view), B = Q  (MN-major)      M128 N64 K128
-//   dQ: A = dS   (K-major),       B = K  (MN-major)      M128 N64 K128
-// TMEM: S 128 + dP 128 + dQ 64 + dK 64 + dV 64 = 448 of 512 columns.
+// Work item = (sequence, head, 128-key tile) along the length-bucketed plan; the CTA walks
+// the sequence's query tiles.  The transposed products put the key on the TMEM lane, so
+// P~^T and dS^T are already the A operands of dV and dK and never leave TMEM (TS MMA); only
+// dS goes to smem, for dQ.
+//
+// CTA = 10 warps (1 per SM):
+//   warps 0-7  two compute warpgroups: thread r of warpgroup x owns key row r and query
+//              columns [64x, 64x+64) of S^T / dP^T; it also stages its half of dQ
+//   warp 8     TMA producer (K, V per item, double-buffered; Q, dO per query tile, 2 stages)
+//              + the LSE / Delta vectors of the query tile into smem (all 32 lanes)
+//   warp 9     TMEM allocator, then MMA issuer (one thread)
+// TMEM columns: S^T 0..127, dP^T 128..255, P~^T 256..319 (bf16 pairs), dS^T 320..383
+// (bf16 pairs; dQ_i = dS K is written over it after dK_i has read it -- tcgen05.mma ops of
+// one thread execute in issue order), dV 384..447, dK 448..511.
+// The MMA issues S_{i+1}, dP_{i+1} as soon as the compute warps have loaded S_i, dP_i, so
+// the exp/dS phase of tile i overlaps the tensor work of tile i+1.
+// dQ_i leaves through smem staging (128-B swizzle) and cp.reduce.async.bulk.tensor add into
+// an fp32 [H*T, 64] accumulator: one TMA op per 32 columns instead of 8192 atomics.
 #include <cmath>
 
 #include "fmha_common.cuh"
@@ -27,19 +36,21 @@ namespace bwd {
 constexpr int kD = 64;
 constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
 constexpr uint32_t kPBytes = kTile * kTile * 2;   // 32 KB
-constexpr int kThreads = 256;
-constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDK = 320, kColDV = 384;
+constexpr int kThreads = 320;
+constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDS = 320, kColDQ = 320, kColDV = 384, kColDK = 448;
 
 struct Smem {
-  uint8_t k[kTileBytes];
-  uint8_t v[kTileBytes];
+  uint8_t k[2][kTileBytes];
+  uint8_t v[2][kTileBytes];
   uint8_t q[2][kTileBytes];
   uint8_t dO[2][kTileBytes];
-  uint8_t p[kPBytes];
-  uint8_t ds[kPBytes];
-  uint64_t kv_full, kv_empty;
+  uint8_t ds[kPBytes];              // dS^T [key][query], 2 x 64-query SW128 regions
+  uint8_t dq[2][kTile * 128];       // dQ staging per warpgroup: [128 rows][32 fp32] SW128
+  float lse2[2][kTile];             // LSE * log2(e) per query row (+inf past the sequence)
+  float delta[2][kTile];
+  uint64_t kv_full[2], kv_empty[2];
   uint64_t qdo_full[2], qdo_empty[2];
-  uint64_t s_full, s_free, ds_full, pds_empty, dq_full, dq_free, dkv_full, dkv_free;
+  uint64_t s_full, s_free, pds_full, pds_empty, dkv_full, dkv_free;
   uint32_t tmem_base;
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
@@ -49,7 +60,6 @@ struct Params {
   FmhaPlanView plan;
   const float* lse;     // [H, T]
   const float* delta;   // [H, T]
-  float* dq_acc;        // [T, H, 64] fp32
   __nv_bfloat16* dqkv;  // [T, 3, H, 64]
   int32_t B, H;
   int64_t T;
@@ -58,299 +68,334 @@ struct Params {
   uint32_t thr, k0, k1, off;
 };
 
-constexpr uint32_t kIdescS = idesc_bf16_f32(128, 128, 0, 0);     // S, dP: K-major x K-major
-constexpr uint32_t kIdescT = idesc_bf16_f32(128, 64, 1, 1);      // dV, dK: A MN-major, B MN-major
-constexpr uint32_t kIdescQ = idesc_bf16_f32(128, 64, 0, 1);      // dQ: A K-major, B MN-major
+constexpr uint32_t kIdescS = idesc_bf16_f32(128, 128, 0, 0);     // S^T, dP^T: K-major x K-major
+constexpr uint32_t kIdescTS = idesc_bf16_f32(128, 64, 0, 1);     // dV, dK: A in TMEM, B MN-major
+constexpr uint32_t kIdescQ = idesc_bf16_f32(128, 64, 1, 1);      // dQ: A MN-major, B MN-major
 
+// keep bits of 8 query columns [q0, q0+8) for this thread's key (lane-cooperative Philox):
+// lane l computes the mask word of key group (l/8) at column q0 + (l%8); lanes then gather
+// bit (l%8) of their group's 8 words.
+__device__ __forceinline__ uint32_t keep8_cols(uint32_t key_grp_j0, uint32_t t_q0, uint32_t h, const Params& prm,
+                                               uint32_t lane) {
+  const uint32_t word = keep_bits8(key_grp_j0, t_q0 + (lane & 7), h, prm.off, prm.k0, prm.k1, prm.thr);
+  uint32_t bits = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t w = __shfl_sync(0xffffffffu, word, (lane & ~7u) + k);
+    bits |= ((w >> (lane & 7)) & 1u) << k;
+  }
+  return bits;
+}
+
+template <bool kDropout>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_constant__ CUtensorMap tmap_do,
-                const Params prm) {
+                const __grid_constant__ CUtensorMap tmap_dq, const Params prm) {
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
     tma_prefetch_desc(&tmap_do);
-    mbar_init(&sm.kv_full, 1);
-    mbar_init(&sm.kv_empty, 1);
+    tma_prefetch_desc(&tmap_dq);
     for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.kv_full[s], 1);
+      mbar_init(&sm.kv_empty[s], 1);
       mbar_init(&sm.qdo_full[s], 1);
       mbar_init(&sm.qdo_empty[s], 1);
     }
     mbar_init(&sm.s_full, 1);
-    mbar_init(&sm.s_free, 4);
-    mbar_init(&sm.ds_full, 4);
+    mbar_init(&sm.s_free, 8);
+    mbar_init(&sm.pds_full, 8);
     mbar_init(&sm.pds_empty, 1);
-    mbar_init(&sm.dq_full, 1);
-    mbar_init(&sm.dq_free, 4);
     mbar_init(&sm.dkv_full, 1);
-    mbar_init(&sm.dkv_free, 4);
+    mbar_init(&sm.dkv_free, 8);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(&sm.tmem_base, 512);
+  if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const int32_t H = prm.H;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t kv_uses = 0, qit = 0;
-      WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, it); w += gridDim.x) {
-        mbar_wait(&sm.kv_empty, (kv_uses & 1) ^ 1);
-        mbar_expect_tx(&sm.kv_full, 2 * kTileBytes);
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer
+    uint32_t items = 0, qit = 0;
+    WorkItem it;
+    for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+      const uint32_t kvs = items & 1;
+      if (lane == 0) {
+        mbar_wait(&sm.kv_empty[kvs], ((items >> 1) & 1) ^ 1);
+        mbar_expect_tx(&sm.kv_full[kvs], 2 * kTileBytes);
         const int32_t krow = it.c0 + it.tile * kTile;
-        tma_load_2d(sm.k, &tmap_qkv, &sm.kv_full, (H + it.h) * kD, krow);
-        tma_load_2d(sm.v, &tmap_qkv, &sm.kv_full, (2 * H + it.h) * kD, krow);
-        ++kv_uses;
-        for (int32_t i = 0; i < it.nt; ++i, ++qit) {
-          const uint32_t st = qit & 1, ph = (qit >> 1) & 1;
-          mbar_wait(&sm.qdo_empty[st], ph ^ 1);
+        tma_load_2d(sm.k[kvs], &tmap_qkv, &sm.kv_full[kvs], (H + it.h) * kD, krow);
+        tma_load_2d(sm.v[kvs], &tmap_qkv, &sm.kv_full[kvs], (2 * H + it.h) * kD, krow);
+      }
+      for (int32_t i = 0; i < it.nt; ++i, ++qit) {
+        const uint32_t st = qit & 1;
+        mbar_wait(&sm.qdo_empty[st], ((qit >> 1) & 1) ^ 1);
+        for (int k = (int)lane; k < kTile; k += 32) {
+          const int32_t row = i * kTile + k;
+          const bool ok = row < it.L;
+          const int64_t t = (int64_t)it.c0 + row;
+          sm.lse2[st][k] = ok ? prm.lse[(int64_t)it.h * prm.T + t] * 1.4426950408889634f : INFINITY;
+          sm.delta[st][k] = ok ? prm.delta[(int64_t)it.h * prm.T + t] : 0.f;
+        }
+        __syncwarp();
+        if (lane == 0) {
           mbar_expect_tx(&sm.qdo_full[st], 2 * kTileBytes);
           tma_load_2d(sm.q[st], &tmap_qkv, &sm.qdo_full[st], it.h * kD, it.c0 + i * kTile);
           tma_load_2d(sm.dO[st], &tmap_do, &sm.qdo_full[st], it.h * kD, it.c0 + i * kTile);
         }
+        __syncwarp();
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      uint32_t kv_uses = 0, qit = 0, s_uses = 0, g_uses = 0, items = 0;
-      const uint32_t k_addr = smem_u32(sm.k), v_addr = smem_u32(sm.v);
-      const uint32_t p_addr = smem_u32(sm.p), ds_addr = smem_u32(sm.ds);
-      auto issue_grads = [&](uint32_t st, bool first) {
-        mbar_wait(&sm.ds_full, g_uses & 1);
-        mbar_wait(&sm.dq_free, (g_uses & 1) ^ 1);
-        if (first) mbar_wait(&sm.dkv_free, (items & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
-#pragma unroll
-        for (uint32_t k = 0; k < kTile / 16; ++k) {        // K = query rows, 16 per MMA
-          const uint64_t pa = sdesc_sw128(p_addr + k * 2048, kTile * 128, 1024);     // P~^T, MN-major
-          const uint64_t da = sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024);    // dS^T, MN-major
-          const uint64_t ob = sdesc_sw128(do_addr + k * 2048, 8192, 1024);           // dO, MN-major
-          const uint64_t qb = sdesc_sw128(q_addr + k * 2048, 8192, 1024);            // Q, MN-major
-          const uint32_t acc = (first && k == 0) ? 0u : 1u;
-          umma_bf16_ss(tmem + kColDV, pa, ob, kIdescT, acc);
-          umma_bf16_ss(tmem + kColDK, da, qb, kIdescT, acc);
-        }
-#pragma unroll
-        for (uint32_t k = 0; k < kTile / 16; ++k) {        // K = key rows, 16 per MMA
-          const uint64_t a = sdesc_sw128(ds_addr + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024);  // dS, K-major
-          const uint64_t b = sdesc_sw128(k_addr + k * 2048, 8192, 1024);                              // K, MN-major
-          umma_bf16_ss(tmem + kColDQ, a, b, kIdescQ, k > 0);
-        }
-        umma_commit(&sm.dq_full);
-        umma_commit(&sm.pds_empty);
-        umma_commit(&sm.qdo_empty[st]);
-        ++g_uses;
-      };
+      uint32_t items = 0, qit = 0, s_cnt = 0, g_cnt = 0;
+      const uint32_t ds_addr = smem_u32(sm.ds);
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, it); w += gridDim.x) {
-        mbar_wait(&sm.kv_full, kv_uses & 1);
+      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+        const uint32_t kvs = items & 1;
+        const uint32_t k_addr = smem_u32(sm.k[kvs]), v_addr = smem_u32(sm.v[kvs]);
+        mbar_wait(&sm.kv_full[kvs], (items >> 1) & 1);
+        auto grads = [&](uint32_t st, bool first) {
+          mbar_wait(&sm.pds_full, g_cnt & 1);
+          if (first) mbar_wait(&sm.dkv_free, (items & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
+#pragma unroll
+          for (uint32_t k = 0; k < kTile / 16; ++k)        // K = query rows, 16 per MMA
+            umma_bf16_ts(tmem + kColDV, tmem + kColP + k * 8, sdesc_sw128(do_addr + k * 2048, 8192, 1024), kIdescTS,
+                         (first && k == 0) ? 0u : 1u);
+#pragma unroll
+          for (uint32_t k = 0; k < kTile / 16; ++k)
+            umma_bf16_ts(tmem + kColDK, tmem + kColDS + k * 8, sdesc_sw128(q_addr + k * 2048, 8192, 1024), kIdescTS,
+                         (first && k == 0) ? 0u : 1u);
+#pragma unroll
+          for (uint32_t k = 0; k < kTile / 16; ++k)        // K = key rows, 16 per MMA
+            umma_bf16_ss(tmem + kColDQ, sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024),
+                         sdesc_sw128(k_addr + k * 2048, 8192, 1024), kIdescQ, k > 0);
+          umma_commit(&sm.pds_empty);
+          umma_commit(&sm.qdo_empty[st]);
+          ++g_cnt;
+        };
         uint32_t prev_st = 0;
         for (int32_t i = 0; i < it.nt; ++i, ++qit) {
-          const uint32_t st = qit & 1, ph = (qit >> 1) & 1;
-          mbar_wait(&sm.qdo_full[st], ph);
-          mbar_wait(&sm.s_free, (s_uses & 1) ^ 1);
+          const uint32_t st = qit & 1;
+          mbar_wait(&sm.qdo_full[st], (qit >> 1) & 1);
+          mbar_wait(&sm.s_free, (s_cnt & 1) ^ 1);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
           for (uint32_t k = 0; k < kD / 16; ++k) {
-            umma_bf16_ss(tmem + kColS, sdesc_sw128(q_addr + k * 32, 16, 1024), sdesc_sw128(k_addr + k * 32, 16, 1024),
+            umma_bf16_ss(tmem + kColS, sdesc_sw128(k_addr + k * 32, 16, 1024), sdesc_sw128(q_addr + k * 32, 16, 1024),
                          kIdescS, k > 0);
-            umma_bf16_ss(tmem + kColDP, sdesc_sw128(do_addr + k * 32, 16, 1024),
-                         sdesc_sw128(v_addr + k * 32, 16, 1024), kIdescS, k > 0);
+            umma_bf16_ss(tmem + kColDP, sdesc_sw128(v_addr + k * 32, 16, 1024),
+                         sdesc_sw128(do_addr + k * 32, 16, 1024), kIdescS, k > 0);
           }
           umma_commit(&sm.s_full);
-          ++s_uses;
-          if (i > 0) issue_grads(prev_st, i == 1);
+          ++s_cnt;
+          if (i > 0) grads(prev_st, i == 1);
           prev_st = st;
         }
-        issue_grads(prev_st, it.nt == 1);
-        umma_commit(&sm.kv_empty);
+        grads(prev_st, it.nt == 1);
+        umma_commit(&sm.kv_empty[kvs]);
         umma_commit(&sm.dkv_full);
-        ++kv_uses;
-        ++items;
       }
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax-grad + epilogues
-    const uint32_t r = threadIdx.x - 128;
+  } else {
+    // ------------------------------------------------------------ compute warpgroups
+    const uint32_t x = warp >> 2;                           // query-column half
+    const uint32_t r = threadIdx.x & 127u;                  // key row (TMEM lane)
     const uint32_t t_row = tmem + (((warp & 3) * 32) << 16);
     const float c = prm.scale_log2;
-    const uint32_t p_addr = smem_u32(sm.p), ds_addr = smem_u32(sm.ds);
-    uint32_t s_uses = 0, g_uses = 0, dq_uses = 0, items = 0;
+    const uint64_t c2 = f2pack(c, c);
+    const uint32_t ds_addr = smem_u32(sm.ds) + x * (kTile * 128);
+    const uint32_t dq_addr = smem_u32(sm.dq[x]);
+    uint32_t s_cnt = 0, g_cnt = 0, qit = 0, items = 0;
+    bool has_prev = false;
+    int32_t prev_row0 = 0;                                  // dQ accumulator row of the pending tile
     WorkItem it;
-    for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, it); w += gridDim.x) {
-      const int32_t kbase = it.tile * kTile;               // first key of this item
-      int32_t prev_row = -1;
 
-      auto consume_dq = [&](int32_t row) {
-        mbar_wait(&sm.dq_full, dq_uses & 1);
+    auto dq_epilogue = [&](int32_t row0) {
+      // pds_empty (waited by the caller) means dQ of the previous tile sits in TMEM
+      uint32_t d[32];
+      tmem_ld32(t_row + kColDQ + x * 32, d);
+      tmem_ld_wait();
+      if (threadIdx.x == 128u * x) bulk_wait_group_read0();   // staging buffer free again
+      named_bar_sync(1 + x, 128);
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        st_shared_v4(dq_addr + sw128_off(r, g), d[4 * g], d[4 * g + 1], d[4 * g + 2], d[4 * g + 3]);
+      fence_proxy_async_smem();
+      named_bar_sync(1 + x, 128);
+      if (threadIdx.x == 128u * x) {
+        tma_reduce_add_2d(&tmap_dq, sm.dq[x], (int32_t)(x * 32), row0);
+        bulk_commit_group();
+      }
+    };
+
+    for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+      const int32_t key = it.tile * kTile + (int32_t)r;
+      const bool key_ok = key < it.L;
+      const uint32_t grp_j0 = (uint32_t)(it.tile * kTile) + (warp & 3) * 32 + (lane & ~7u);
+      for (int32_t i = 0; i < it.nt; ++i, ++qit) {
+        const uint32_t st = qit & 1;
+        mbar_wait(&sm.qdo_full[st], (qit >> 1) & 1);     // LSE / Delta of this query tile
+        mbar_wait(&sm.s_full, s_cnt & 1);
         tc_fence_after();
-        uint32_t a0[32], a1[32];
-        tmem_ld32(t_row + kColDQ, a0);
-        tmem_ld32(t_row + kColDQ + 32, a1);
+        uint32_t sr[2][32], dr[2][32];
+        tmem_ld32(t_row + kColS + x * 64, sr[0]);
+        tmem_ld32(t_row + kColS + x * 64 + 32, sr[1]);
+        tmem_ld32(t_row + kColDP + x * 64, dr[0]);
+        tmem_ld32(t_row + kColDP + x * 64 + 32, dr[1]);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.dq_free);
-        ++dq_uses;
-        if (row < it.L) {
-          float4* dst = reinterpret_cast<float4*>(prm.dq_acc + ((int64_t)(it.c0 + row) * H + it.h) * kD);
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            atomicAdd(dst + g, make_float4(__uint_as_float(a0[4 * g]), __uint_as_float(a0[4 * g + 1]),
-                                           __uint_as_float(a0[4 * g + 2]), __uint_as_float(a0[4 * g + 3])));
-            atomicAdd(dst + 8 + g, make_float4(__uint_as_float(a1[4 * g]), __uint_as_float(a1[4 * g + 1]),
-                                               __uint_as_float(a1[4 * g + 2]), __uint_as_float(a1[4 * g + 3])));
-          }
-        }
-      };
+        if (lane == 0) mbar_arrive(&sm.s_free);
+        ++s_cnt;
 
-      for (int32_t i = 0; i < it.nt; ++i) {
-        const int32_t row = i * kTile + (int32_t)r;          // query row inside the sequence
-        const bool row_ok = row < it.L;
-        const uint32_t t_glob = (uint32_t)(it.c0 + row);
-        const float lse2 = row_ok ? prm.lse[(int64_t)it.h * prm.T + t_glob] * 1.4426950408889634f : INFINITY;
-        const float dl = row_ok ? prm.delta[(int64_t)it.h * prm.T + t_glob] : 0.f;
-        mbar_wait(&sm.s_full, s_uses & 1);
-        tc_fence_after();
-        mbar_wait(&sm.pds_empty, (g_uses & 1) ^ 1);
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ++ch) {
-          uint32_t sr[32], dr[32];
-          tmem_ld32(t_row + kColS + ch * 32, sr);
-          tmem_ld32(t_row + kColDP + ch * 32, dr);
-          tmem_ld_wait();
-          const int32_t key0 = kbase + ch * 32;
+        uint32_t pp[32], pd[32];
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const int q0 = (int)x * 64 + ch * 32;
           uint32_t keep = 0xFFFFFFFFu;
-          if (prm.thr != 0) {
+          if (kDropout) {
             keep = 0;
+            const uint32_t tq = (uint32_t)(it.c0 + i * kTile + q0);
 #pragma unroll
-            for (int g = 0; g < 4; ++g)
-              keep |= keep_bits8(key0 + g * 8, t_glob, it.h, prm.off, prm.k0, prm.k1, prm.thr) << (8 * g);
-          }
-          float pd[32], ds[32];
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const bool kv = key0 + e < it.L;
-            const float P = kv ? ex2f(fmaf(__uint_as_float(sr[e]), c, -lse2)) : 0.f;
-            const bool kp = (keep >> e) & 1u;
-            const float dp = kp ? __uint_as_float(dr[e]) * prm.rp : 0.f;
-            pd[e] = kp ? P * prm.rp : 0.f;
-            ds[e] = P * (dp - dl);
+            for (int b8 = 0; b8 < 4; ++b8) keep |= keep8_cols(grp_j0, tq + 8 * b8, it.h, prm, lane) << (8 * b8);
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t unit = (ch & 1) * 4 + u, region = (ch >> 1) * (kTile * 128);
-            const uint32_t off = region + sw128_off(r, unit);
-            st_shared_v4(p_addr + off, pack_bf16(pd[8 * u], pd[8 * u + 1]), pack_bf16(pd[8 * u + 2], pd[8 * u + 3]),
-                         pack_bf16(pd[8 * u + 4], pd[8 * u + 5]), pack_bf16(pd[8 * u + 6], pd[8 * u + 7]));
-            st_shared_v4(ds_addr + off, pack_bf16(ds[8 * u], ds[8 * u + 1]), pack_bf16(ds[8 * u + 2], ds[8 * u + 3]),
-                         pack_bf16(ds[8 * u + 4], ds[8 * u + 5]), pack_bf16(ds[8 * u + 6], ds[8 * u + 7]));
+          for (int e = 0; e < 32; e += 2) {
+            const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse2[st][q0 + e]);
+            const float2 dl = *reinterpret_cast<const float2*>(&sm.delta[st][q0 + e]);
+            float pa, pb;
+            f2unpack(ffma2(f2pack(__uint_as_float(sr[ch][e]), __uint_as_float(sr[ch][e + 1])), c2,
+                           f2pack(-l2.x, -l2.y)), pa, pb);
+            pa = key_ok ? ex2f(pa) : 0.f;
+            pb = key_ok ? ex2f(pb) : 0.f;
+            float dpa = __uint_as_float(dr[ch][e]), dpb = __uint_as_float(dr[ch][e + 1]);
+            float qa = pa, qb = pb;
+            if (kDropout) {
+              const bool ka = (keep >> e) & 1u, kb = (keep >> (e + 1)) & 1u;
+              qa = ka ? pa * prm.rp : 0.f;
+              qb = kb ? pb * prm.rp : 0.f;
+              dpa = ka ? dpa * prm.rp : 0.f;
+              dpb = kb ? dpb * prm.rp : 0.f;
+            }
+            float da, db;
+            f2unpack(fmul2(f2pack(pa, pb), fadd2(f2pack(dpa, dpb), f2pack(-dl.x, -dl.y))), da, db);
+            pp[ch * 16 + e / 2] = pack_bf16(qa, qb);
+            pd[ch * 16 + e / 2] = pack_bf16(da, db);
           }
         }
-        tc_fence_before();
+        // grads of the previous tile done: P~^T / dS^T TMEM and dS smem are free, dQ ready
+        mbar_wait(&sm.pds_empty, (g_cnt & 1) ^ 1);
+        tc_fence_after();
+        if (has_prev) dq_epilogue(prev_row0);
+        tmem_st32(t_row + kColP + x * 32, pp);
+        tmem_st32(t_row + kColDS + x * 32, pd);
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          st_shared_v4(ds_addr + sw128_off(r, g), pd[4 * g], pd[4 * g + 1], pd[4 * g + 2], pd[4 * g + 3]);
+        tmem_st_wait();
         fence_proxy_async_smem();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&sm.s_free);
-          mbar_arrive(&sm.ds_full);
-        }
-        ++s_uses;
-        ++g_uses;
-        if (i > 0) consume_dq(prev_row);
-        prev_row = row;
+        if (lane == 0) mbar_arrive(&sm.pds_full);
+        ++g_cnt;
+        has_prev = true;
+        prev_row0 = (int32_t)((int64_t)it.h * prm.T + it.c0 + i * kTile);
       }
-      consume_dq(prev_row);
-
-      // dK, dV epilogue: thread r owns key row kbase + r
+      // dK, dV of this key tile
       mbar_wait(&sm.dkv_full, items & 1);
       tc_fence_after();
       uint32_t kr[32], vr[32];
-      const int32_t key = kbase + (int32_t)r;
-      const int64_t t = (int64_t)it.c0 + key;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        tmem_ld32(t_row + kColDK + half * 32, kr);
-        tmem_ld32(t_row + kColDV + half * 32, vr);
-        tmem_ld_wait();
-        if (key < it.L) {
-          uint4* dk = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 1) * H + it.h) * kD + half * 32);
-          uint4* dv = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 2) * H + it.h) * kD + half * 32);
-#pragma unroll
-          for (int g = 0; g < 4; ++g) {
-            const float s = prm.scale;
-            dk[g] = make_uint4(pack_bf16(__uint_as_float(kr[8 * g]) * s, __uint_as_float(kr[8 * g + 1]) * s),
-                               pack_bf16(__uint_as_float(kr[8 * g + 2]) * s, __uint_as_float(kr[8 * g + 3]) * s),
-                               pack_bf16(__uint_as_float(kr[8 * g + 4]) * s, __uint_as_float(kr[8 * g + 5]) * s),
-                               pack_bf16(__uint_as_float(kr[8 * g + 6]) * s, __uint_as_float(kr[8 * g + 7]) * s));
-            dv[g] = make_uint4(pack_bf16(__uint_as_float(vr[8 * g]), __uint_as_float(vr[8 * g + 1])),
-                               pack_bf16(__uint_as_float(vr[8 * g + 2]), __uint_as_float(vr[8 * g + 3])),
-                               pack_bf16(__uint_as_float(vr[8 * g + 4]), __uint_as_float(vr[8 * g + 5])),
-                               pack_bf16(__uint_as_float(vr[8 * g + 6]), __uint_as_float(vr[8 * g + 7])));
-          }
-        }
-      }
+      tmem_ld32(t_row + kColDK + x * 32, kr);
+      tmem_ld32(t_row + kColDV + x * 32, vr);
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.dkv_free);
-      ++items;
+      if (key_ok) {
+        const int64_t t = (int64_t)it.c0 + key;
+        uint4* dk = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 1) * H + it.h) * kD + x * 32);
+        uint4* dv = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 2) * H + it.h) * kD + x * 32);
+        const float sc = prm.scale;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          dk[g] = make_uint4(pack_bf16(__uint_as_float(kr[8 * g]) * sc, __uint_as_float(kr[8 * g + 1]) * sc),
+                             pack_bf16(__uint_as_float(kr[8 * g + 2]) * sc, __uint_as_float(kr[8 * g + 3]) * sc),
+                             pack_bf16(__uint_as_float(kr[8 * g + 4]) * sc, __uint_as_float(kr[8 * g + 5]) * sc),
+                             pack_bf16(__uint_as_float(kr[8 * g + 6]) * sc, __uint_as_float(kr[8 * g + 7]) * sc));
+          dv[g] = make_uint4(pack_bf16(__uint_as_float(vr[8 * g]), __uint_as_float(vr[8 * g + 1])),
+                             pack_bf16(__uint_as_float(vr[8 * g + 2]), __uint_as_float(vr[8 * g + 3])),
+                             pack_bf16(__uint_as_float(vr[8 * g + 4]), __uint_as_float(vr[8 * g + 5])),
+                             pack_bf16(__uint_as_float(vr[8 * g + 6]), __uint_as_float(vr[8 * g + 7])));
+        }
+      }
     }
+    if (has_prev) {
+      mbar_wait(&sm.pds_empty, (g_cnt & 1) ^ 1);
+      tc_fence_after();
+      dq_epilogue(prev_row0);
+    }
+    if (threadIdx.x == 128u * x) bulk_wait_group0();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
 }
 
-// Prologue: Delta[h, t] = sum_d O[t,h,d] dO[t,h,d]; dq_acc[t,h,:] = 0.  Block 0 / warp 0
-// additionally builds the length-bucketed plan (fmha_plan.cu semantics).
+// Prologue: Delta[h, t] = sum_d O[t,h,d] dO[t,h,d]  (8 threads per (t, h) row, 16-B loads)
+// and dq_acc = 0 (grid-stride float4 stores).
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ out,
                                                       const __nv_bfloat16* __restrict__ dout, float* __restrict__ delta,
-                                                      float* __restrict__ dq_acc, int64_t T, int32_t H) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // row (t, h)
-  if (idx >= T * H) return;
-  const uint4* o = reinterpret_cast<const uint4*>(out + idx * kD);
-  const uint4* g = reinterpret_cast<const uint4*>(dout + idx * kD);
-  float s = 0.f;
-#pragma unroll
-  for (int k = 0; k < kD / 8; ++k) {
-    const uint4 a = o[k], b = g[k];
+                                                      float4* __restrict__ dq_acc, int64_t T, int32_t H, int64_t n_acc4) {
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gtid >> 3;                   // (t, h) row
+  const int part = (int)(gtid & 7);
+  if (row < T * H) {
+    const uint4 a = reinterpret_cast<const uint4*>(out + row * kD)[part];
+    const uint4 b = reinterpret_cast<const uint4*>(dout + row * kD)[part];
     const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+    float s = 0.f;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       s = fmaf(__uint_as_float(av[e] << 16), __uint_as_float(bv[e] << 16), s);
       s = fmaf(__uint_as_float(av[e] & 0xFFFF0000u), __uint_as_float(bv[e] & 0xFFFF0000u), s);
     }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (part == 0) {
+      const int64_t t = row / H;
+      const int32_t h = (int32_t)(row - t * H);
+      delta[(int64_t)h * T + t] = s;
+    }
   }
-  const int64_t t = idx / H;
-  const int32_t h = (int32_t)(idx - t * H);
-  delta[(int64_t)h * T + t] = s;
-  float4* acc = reinterpret_cast<float4*>(dq_acc + idx * kD);
-#pragma unroll
-  for (int k = 0; k < kD / 4; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t k = gtid; k < n_acc4; k += (int64_t)gridDim.x * blockDim.x) dq_acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-// Epilogue: dQ (bf16) = scale * dq_acc into dqkv[:, 0].
+// Finalize: dqkv[t, 0, h, :] = bf16(scale * dq_acc[h * T + t, :]).
 __global__ void __launch_bounds__(256) bwd_dq_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv,
                                                      int64_t T, int32_t H, float scale) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (t, h, 8-wide group)
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // (h, t, 8-wide group)
   if (idx >= T * H * (kD / 8)) return;
-  const int64_t row = idx / (kD / 8);
-  const int32_t g = (int32_t)(idx - row * (kD / 8));
-  const int64_t t = row / H;
-  const int32_t h = (int32_t)(row - t * H);
+  const int64_t row = idx >> 3;                  // h * T + t
+  const int32_t g = (int32_t)(idx & 7);
+  const int32_t h = (int32_t)(row / T);
+  const int64_t t = row - (int64_t)h * T;
   const float4* a = reinterpret_cast<const float4*>(dq_acc + row * kD + g * 8);
   const float4 x = a[0], y = a[1];
   uint4 v = make_uint4(pack_bf16(x.x * scale, x.y * scale), pack_bf16(x.z * scale, x.w * scale),
@@ -366,25 +411,29 @@ size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p) {
 
 ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* out, const float* lse, const void* dout,
                          const int32_t* d_cu, void* dqkv, void* ws, cudaStream_t s) {
-  UB_CHECK_CUDA(cudaFuncSetAttribute(bwd::fmha_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)bwd::kSmemBytes));
-  CUtensorMap tq, tdo;
+  const bool drop = p.p_dropout > 0.f;
+  auto kern = drop ? bwd::fmha_bwd_kernel<true> : bwd::fmha_bwd_kernel<false>;
+  UB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmemBytes));
+  char* base = static_cast<char*>(ws);
+  FmhaPlanView v = fmha_plan_view(base, p.B);
+  char* extra = base + align_up(fmha_plan_bytes(p.B), 256);
+  float* delta = reinterpret_cast<float*>(extra);
+  float* dq_acc = reinterpret_cast<float*>(extra + align_up((size_t)p.T * p.heads * 4, 256));
+  CUtensorMap tq, tdo, tdq;
   ub_status st = make_tmap_bf16(&tq, qkv, (uint64_t)3 * p.heads * bwd::kD, (uint64_t)p.T,
                                 (uint64_t)3 * p.heads * bwd::kD * 2);
   if (st != UB_OK) return st;
   if ((st = make_tmap_bf16(&tdo, dout, (uint64_t)p.heads * bwd::kD, (uint64_t)p.T, (uint64_t)p.heads * bwd::kD * 2)) !=
       UB_OK)
     return st;
-  char* base = static_cast<char*>(ws);
-  FmhaPlanView v = fmha_plan_view(base, p.B);
-  char* extra = base + align_up(fmha_plan_bytes(p.B), 256);
-  float* delta = reinterpret_cast<float*>(extra);
-  float* dq_acc = reinterpret_cast<float*>(extra + align_up((size_t)p.T * p.heads * 4, 256));
+  if ((st = make_tmap_f32(&tdq, dq_acc, bwd::kD, (uint64_t)p.T * p.heads, bwd::kD * 4, 32, kTile)) != UB_OK) return st;
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
-  if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, v, s)) != UB_OK) return st;
+  if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 1, v, s)) != UB_OK) return st;
   const int64_t rows = p.T * p.heads;
-  bwd::bwd_pre_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), delta, dq_acc, p.T, p.heads);
+  const int64_t n_acc4 = rows * bwd::kD / 4;
+  bwd::bwd_pre_kernel<<<(unsigned)((rows * 8 + 255) / 256), 256, 0, s>>>(
+      static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), delta,
+      reinterpret_cast<float4*>(dq_acc), p.T, p.heads, n_acc4);
   UB_CHECK_LAUNCH();
 
   bwd::Params prm{};
@@ -392,7 +441,6 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   prm.plan = v;
   prm.lse = lse;
   prm.delta = delta;
-  prm.dq_acc = dq_acc;
   prm.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   prm.B = p.B;
   prm.H = p.heads;
@@ -400,7 +448,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   prm.scale = p.scale;
   prm.scale_log2 = p.scale * 1.4426950408889634f;
   prm.rp = 1.f / (1.f - p.p_dropout);
-  prm.thr = p.p_dropout > 0.f ? (uint32_t)floor((double)p.p_dropout * 65536.0) : 0u;
+  prm.thr = drop ? (uint32_t)floor((double)p.p_dropout * 65536.0) : 0u;
   prm.k0 = (uint32_t)(p.seed & 0xFFFFFFFFull);
   prm.k1 = (uint32_t)(p.seed >> 32);
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
@@ -411,7 +459,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfBwd, 0, s);
-  bwd::fmha_bwd_kernel<<<grid, bwd::kThreads, bwd::kSmemBytes, s>>>(tq, tdo, prm);
+  kern<<<grid, bwd::kThreads, bwd::kSmemBytes, s>>>(tq, tdo, tdq, prm);
   UB_CHECK_LAUNCH();
   prof_record(kProfBwd, 1, s);
   const int64_t n = rows * (bwd::kD / 8);

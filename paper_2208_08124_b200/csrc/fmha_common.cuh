@@ -10,12 +10,12 @@
 namespace ub {
 
 struct WorkItem {
-  int32_t b, h, tile, c0, L, nt;
+  int32_t b, h, tile, c0, L, nt, ntile;   // tile = first tile of the item, ntile = tiles in it
 };
 
-// Map a flat work index onto (sequence, head, tile) along the bucketed plan.
+// Map a flat work index onto (sequence, head, tile group) along the bucketed plan.
 __device__ __forceinline__ bool decode_item(int32_t w, const FmhaPlanView& v, const int32_t* __restrict__ cu,
-                                            int32_t B, int32_t H, WorkItem& it) {
+                                            int32_t B, int32_t H, int32_t tiles_per_item, WorkItem& it) {
   const int32_t total = v.item_prefix[B];
   if (w >= total) return false;
   int32_t lo = 0, hi = B;                       // largest k with prefix[k] <= w
@@ -28,8 +28,10 @@ __device__ __forceinline__ bool decode_item(int32_t w, const FmhaPlanView& v, co
   it.c0 = cu[it.b];
   it.L = cu[it.b + 1] - it.c0;
   it.nt = (it.L + kTile - 1) / kTile;
-  it.h = local / it.nt;
-  it.tile = local - it.h * it.nt;
+  const int32_t ngroups = (it.nt + tiles_per_item - 1) / tiles_per_item;
+  it.h = local / ngroups;
+  it.tile = (local - it.h * ngroups) * tiles_per_item;
+  it.ntile = min(tiles_per_item, it.nt - it.tile);
   return true;
 }
 
@@ -52,5 +54,9 @@ __device__ __forceinline__ uint32_t keep_bits8(uint32_t j0, uint32_t t, uint32_t
 // `pitch_bytes`, box {64 cols, 128 rows}, 128-B swizzle (matches sdesc_sw128).
 ub_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
                          uint32_t box_cols = 64, uint32_t box_rows = 128);
+// Host: 2-D fp32 tensor map (row-major [rows, cols]), box {box_cols, box_rows}, 128-B swizzle
+// (box_cols * 4 must be 128).
+ub_status make_tmap_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
+                        uint32_t box_cols, uint32_t box_rows);
 
 }  // namespace ub

@@ -1,22 +1,31 @@
 // Varlen FMHA forward on B200 tensor cores (tcgen05 + TMEM + TMA), bf16 in, fp32 accumulate.
 //
 // Eq. (1) of the paper per sequence and head on cu_seqlens-packed tokens (P:302,
-// P:313).  One persistent launch walks the length-bucketed plan (fmha_plan.cu).
+// P:313).  One persistent launch walks the length-bucketed plan (fmha_plan.cu);
+// a work item is (sequence, head, pair of 128-row query tiles) so the two query tiles
+// share every K/V tile load.
 //
-// CTA = 8 warps, warp-specialised:
-//   warp 0      TMA producer: Q tile (128 x 64) once per item; K_j, V_j tiles (128 x 64)
-//               through a 2-stage ring, straight from the packed qkv [T, 3*H*64] matrix.
-//   warp 1      MMA issuer (one thread): S_j = Q K_j^T  (M128 N128 K64, K-major x K-major)
-//               into TMEM (double-buffered), then O_j = P_j V_j (M128 N64 K128, P from
-//               smem K-major, V MN-major) into TMEM (double-buffered).
-//   warp 2      TMEM allocator.
-//   warps 4-7   softmax: thread r owns query row r; tcgen05.ld its S row, masks keys past
-//               the sequence end, online max / exp2 / row sum in registers, writes P (bf16)
-//               to smem in the UMMA SW128 layout, and accumulates the per-tile O_j
-//               (relative to the running max) in registers; epilogue writes O and LSE.
+// CTA = 10 warps (1 per SM), warp-specialised:
+//   warps 0-3   softmax warpgroup 0: query tile A (thread r owns row r)
+//   warps 4-7   softmax warpgroup 1: query tile B
+//   warp 8      TMA producer: Q_A, Q_B (double-buffered across items), K_j / V_j through a
+//               3-stage ring, straight from the packed qkv [T, 3*H*64] matrix (128-B swizzle)
+//   warp 9      TMEM allocator, then MMA issuer (one thread):
+//                 S_x(j) = Q_x K_j^T   M128 N128 K64, smem x smem       -> TMEM S_x
+//                 O_x   += P_x(j) V_j  M128 N64 K128, P from TMEM (TS) -> TMEM O_x
+//               issue order S_A(j+1), PV_A(j), S_B(j+1), PV_B(j): the tensor pipe alternates
+//               between the two warpgroups while each runs its exp phase
+// TMEM (512 columns): per warpgroup x: S at 256x (128 cols fp32), P at 256x+128 (64 cols,
+// bf16 pairs), O at 256x+192 (64 cols fp32).
+// Softmax per tile: tcgen05.ld the S row, mask keys past the sequence end, 3-input max
+// tree, exp2 (MUFU, a fraction on the FMA pipe by polynomial), packed f32x2 sums,
+// P -> TMEM by tcgen05.st.  O stays in TMEM; it is rescaled (ld/scale/st) only when the
+// running max grows by more than 2^8 (lazy rescale: P is bounded by 256, exact in the end
+// because l uses the same reference max).
 // Boxes that run past a sequence end read the next sequence's rows: those keys are
 // masked to -inf and those query rows are never stored.
 #include <cmath>
+#include <cstdlib>
 
 #include "fmha_common.cuh"
 
@@ -24,19 +33,18 @@ namespace ub {
 namespace fwd {
 
 constexpr int kD = 64;
-constexpr int kStages = 2;
-constexpr uint32_t kTileBytes = kTile * kD * 2;          // 16 KB
-constexpr uint32_t kPBytes = kTile * kTile * 2;          // 32 KB (2 chunks of 64 keys)
-constexpr int kThreads = 256;
+constexpr int kStages = 3;
+constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
+constexpr int kThreads = 320;
+constexpr float kRescaleThreshold = 8.0f;         // log2 units
 
 struct Smem {
-  uint8_t q[kTileBytes];
+  uint8_t q[2][2][kTileBytes];                    // [item slot][warpgroup]
   uint8_t k[kStages][kTileBytes];
   uint8_t v[kStages][kTileBytes];
-  uint8_t p[2][kPBytes];
-  uint64_t q_full, q_empty;
+  uint64_t q_full[2], q_empty[2];
   uint64_t k_full[kStages], v_full[kStages], kv_empty[kStages];
-  uint64_t s_full[2], s_free[2], p_full[2], p_empty[2], o_full[2], o_free[2];
+  uint64_t s_full[2], s_free[2], p_full[2], o_done[2], o_free[2];   // per warpgroup
   uint32_t tmem_base;
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
@@ -53,9 +61,17 @@ struct Params {
   uint32_t thr, k0, k1, off;
 };
 
-constexpr uint32_t kIdescS = idesc_bf16_f32(128, 128, 0, 0);
-constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, 0, 1);
+constexpr uint32_t kIdescS = idesc_bf16_f32(128, 128, 0, 0);   // Q (K-major) x K (K-major)
+constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 64, 0, 1);   // P (TMEM) x V (MN-major)
+__host__ __device__ constexpr uint32_t col_s(int x) { return 256u * x; }
+__host__ __device__ constexpr uint32_t col_p(int x) { return 256u * x + 128u; }
+__host__ __device__ constexpr uint32_t col_o(int x) { return 256u * x + 192u; }
 
+// kPoly: number of column pairs out of every 8 whose exp2 runs on the FMA pipe (ex2_poly2).
+// kPack: 0 = bf16 packing by cvt (XU pipe), 1 = integer rounding + byte permute.
+// kDropout: compile the Philox mask in (p > 0) or out (p == 0: no RNG code at all, so the
+// compiler cannot hoist it into the exp loop).
+template <int kPoly, int kPack, bool kDropout>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) {
   extern __shared__ uint8_t smem_raw[];
@@ -63,42 +79,44 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
-    mbar_init(&sm.q_full, 1);
-    mbar_init(&sm.q_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&sm.q_full[s], 1);
+      mbar_init(&sm.q_empty[s], 1);
+      mbar_init(&sm.s_full[s], 1);
+      mbar_init(&sm.s_free[s], 4);
+      mbar_init(&sm.p_full[s], 4);
+      mbar_init(&sm.o_done[s], 1);
+      mbar_init(&sm.o_free[s], 4);
+    }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&sm.k_full[s], 1);
       mbar_init(&sm.v_full[s], 1);
       mbar_init(&sm.kv_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&sm.s_full[s], 1);
-      mbar_init(&sm.s_free[s], 4);
-      mbar_init(&sm.p_full[s], 4);
-      mbar_init(&sm.p_empty[s], 1);
-      mbar_init(&sm.o_full[s], 1);
-      mbar_init(&sm.o_free[s], 4);
-    }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(&sm.tmem_base, 512);
+  if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const int32_t H = prm.H;
+  //if (warp >= 8) regs_dec<80>();      // producer / MMA / allocator warpgroup
+  //else regs_inc<208>();               // softmax warpgroups
 
-  if (warp == 0) {
+  if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      uint32_t q_uses = 0, kv_it = 0;
+      uint32_t items = 0, kv_it = 0;
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, it); w += gridDim.x) {
-        mbar_wait(&sm.q_empty, (q_uses & 1) ^ 1);
-        mbar_expect_tx(&sm.q_full, kTileBytes);
-        tma_load_2d(sm.q, &tmap_qkv, &sm.q_full, it.h * kD, it.c0 + it.tile * kTile);
-        ++q_uses;
+      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
+        const uint32_t slot = items & 1;
+        mbar_wait(&sm.q_empty[slot], ((items >> 1) & 1) ^ 1);
+        mbar_expect_tx(&sm.q_full[slot], kTileBytes * it.ntile);
+        for (int x = 0; x < it.ntile; ++x)
+          tma_load_2d(sm.q[slot][x], &tmap_qkv, &sm.q_full[slot], it.h * kD, it.c0 + (it.tile + x) * kTile);
         for (int32_t j = 0; j < it.nt; ++j, ++kv_it) {
           const uint32_t st = kv_it % kStages, ph = (kv_it / kStages) & 1;
           mbar_wait(&sm.kv_empty[st], ph ^ 1);
@@ -109,115 +127,101 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
-      uint32_t q_uses = 0, kv_it = 0, s_it = 0, p_it = 0, o_it = 0;
-      const uint32_t q_addr = smem_u32(sm.q);
-      auto issue_pv = [&](uint32_t st, uint32_t vph) {
-        const uint32_t pb = p_it & 1, ob = o_it & 1;
-        mbar_wait(&sm.p_full[pb], (p_it >> 1) & 1);
-        mbar_wait(&sm.v_full[st], vph);
-        mbar_wait(&sm.o_free[ob], ((o_it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t p_addr = smem_u32(sm.p[pb]), v_addr = smem_u32(sm.v[st]);
-#pragma unroll
-        for (uint32_t k = 0; k < kTile / 16; ++k) {
-          const uint64_t a = sdesc_sw128(p_addr + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = sdesc_sw128(v_addr + k * 2048, 8192, 1024);
-          umma_bf16_ss(tmem + 256 + ob * 64, a, bd, kIdescPV, k > 0);
-        }
-        umma_commit(&sm.o_full[ob]);
-        umma_commit(&sm.p_empty[pb]);
-        umma_commit(&sm.kv_empty[st]);
-        ++p_it;
-        ++o_it;
-      };
+      uint32_t items = 0, kv_it = 0;
+      uint32_t s_cnt[2] = {0, 0}, p_cnt[2] = {0, 0}, it_cnt[2] = {0, 0};
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, it); w += gridDim.x) {
-        mbar_wait(&sm.q_full, q_uses & 1);
+      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
+        const uint32_t slot = items & 1;
+        const int nx = it.ntile;
+        mbar_wait(&sm.q_full[slot], (items >> 1) & 1);
         tc_fence_after();
-        uint32_t prev_st = 0, prev_ph = 0;
-        for (int32_t j = 0; j < it.nt; ++j, ++kv_it) {
-          const uint32_t st = kv_it % kStages, ph = (kv_it / kStages) & 1;
-          mbar_wait(&sm.k_full[st], ph);
-          const uint32_t sb = s_it & 1;
-          mbar_wait(&sm.s_free[sb], ((s_it >> 1) & 1) ^ 1);
+        auto issue_s = [&](int x, uint32_t st) {
+          mbar_wait(&sm.s_free[x], (s_cnt[x] & 1) ^ 1);
           tc_fence_after();
-          const uint32_t k_addr = smem_u32(sm.k[st]);
+          const uint32_t q_addr = smem_u32(sm.q[slot][x]), k_addr = smem_u32(sm.k[st]);
 #pragma unroll
-          for (uint32_t k = 0; k < kD / 16; ++k) {
-            const uint64_t a = sdesc_sw128(q_addr + k * 32, 16, 1024);
-            const uint64_t bd = sdesc_sw128(k_addr + k * 32, 16, 1024);
-            umma_bf16_ss(tmem + sb * 128, a, bd, kIdescS, k > 0);
-          }
-          umma_commit(&sm.s_full[sb]);
-          ++s_it;
-          if (j == it.nt - 1) umma_commit(&sm.q_empty);
-          if (j > 0) issue_pv(prev_st, prev_ph);
-          prev_st = st;
-          prev_ph = ph;
+          for (uint32_t k = 0; k < kD / 16; ++k)
+            umma_bf16_ss(tmem + col_s(x), sdesc_sw128(q_addr + k * 32, 16, 1024), sdesc_sw128(k_addr + k * 32, 16, 1024),
+                         kIdescS, k > 0);
+          umma_commit(&sm.s_full[x]);
+          ++s_cnt[x];
+        };
+        {
+          const uint32_t st0 = kv_it % kStages;
+          mbar_wait(&sm.k_full[st0], (kv_it / kStages) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+            if (x < nx) issue_s(x, st0);
         }
-        issue_pv(prev_st, prev_ph);
-        ++q_uses;
+        for (int32_t j = 0; j < it.nt; ++j) {
+          const uint32_t cur = kv_it + j, st = cur % kStages, ph = (cur / kStages) & 1;
+          const bool has_next = j + 1 < it.nt;
+          const uint32_t nst = (cur + 1) % kStages;
+          if (has_next) {
+            mbar_wait(&sm.k_full[nst], ((cur + 1) / kStages) & 1);
+            tc_fence_after();
+          }
+          mbar_wait(&sm.v_full[st], ph);
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            if (x >= nx) break;
+            if (has_next) issue_s(x, nst);
+            mbar_wait(&sm.p_full[x], p_cnt[x] & 1);
+            if (j == 0) mbar_wait(&sm.o_free[x], (it_cnt[x] & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t v_addr = smem_u32(sm.v[st]);
+#pragma unroll
+            for (uint32_t k = 0; k < kTile / 16; ++k)
+              umma_bf16_ts(tmem + col_o(x), tmem + col_p(x) + k * 8, sdesc_sw128(v_addr + k * 2048, 8192, 1024),
+                           kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&sm.o_done[x]);
+            ++p_cnt[x];
+          }
+          umma_commit(&sm.kv_empty[st]);
+        }
+        umma_commit(&sm.q_empty[slot]);
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+          if (x < nx) ++it_cnt[x];
+        kv_it += it.nt;
       }
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax + epilogue
-    const uint32_t r = threadIdx.x - 128;                 // query row inside the tile
-    const uint32_t lane_base = (warp & 3) * 32;           // TMEM sub-partition of this warp
-    const uint32_t t_row = tmem + (lane_base << 16);
+  } else if (warp < 8) {
+    // ------------------------------------------------------------ softmax warpgroups
+    const int x = (int)(warp >> 2);                       // warpgroup / query tile of the pair
+    const uint32_t r = threadIdx.x - 128u * x;            // row inside the tile
+    const uint32_t t_row = tmem + (((warp & 3) * 32) << 16);
     const float c = prm.scale_log2;
-    uint32_t s_it = 0, p_it = 0, o_it = 0;
+    const uint64_t c2 = f2pack(c, c);
+    uint32_t s_cnt = 0, pv_cnt = 0;
     WorkItem it;
-    for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, it); w += gridDim.x) {
-      const int32_t row = it.tile * kTile + (int32_t)r;
+    for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x) {
+      if (x >= it.ntile) continue;
+      const int32_t row = (it.tile + x) * kTile + (int32_t)r;
       const uint32_t t_glob = (uint32_t)(it.c0 + row);
-      float m = -INFINITY, l = 0.f, m_acc = -INFINITY, m_tile = -INFINITY;
-      float acc[kD];
-#pragma unroll
-      for (int d = 0; d < kD; ++d) acc[d] = 0.f;
-
-      auto consume_o = [&](float mj) {
-        const uint32_t ob = o_it & 1;
-        mbar_wait(&sm.o_full[ob], (o_it >> 1) & 1);
-        tc_fence_after();
-        uint32_t o0[32], o1[32];
-        tmem_ld32(t_row + 256 + ob * 64, o0);
-        tmem_ld32(t_row + 256 + ob * 64 + 32, o1);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.o_free[ob]);
-        ++o_it;
-        const float f = ex2f((m_acc - mj) * c);
-#pragma unroll
-        for (int d = 0; d < 32; ++d) {
-          acc[d] = fmaf(acc[d], f, __uint_as_float(o0[d]));
-          acc[32 + d] = fmaf(acc[32 + d], f, __uint_as_float(o1[d]));
-        }
-        m_acc = mj;
-      };
-
+      float m_run = -INFINITY, l = 0.f;
       for (int32_t j = 0; j < it.nt; ++j) {
-        const uint32_t sb = s_it & 1;
-        mbar_wait(&sm.s_full[sb], (s_it >> 1) & 1);
+        mbar_wait(&sm.s_full[x], s_cnt & 1);
         tc_fence_after();
         float s[kTile];
         {
-          uint32_t raw[32];
+          uint32_t raw[4][32];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            tmem_ld32(t_row + sb * 128 + q * 32, raw);
-            tmem_ld_wait();
+          for (int q = 0; q < 4; ++q) tmem_ld32(t_row + col_s(x) + q * 32, raw[q]);
+          tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) s[q * 32 + e] = __uint_as_float(raw[e]);
-          }
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int e = 0; e < 32; ++e) s[q * 32 + e] = __uint_as_float(raw[q][e]);
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.s_free[sb]);
-        ++s_it;
+        if (lane == 0) mbar_arrive(&sm.s_free[x]);
+        ++s_cnt;
 
         const int32_t kvalid = it.L - j * kTile;
         if (kvalid < kTile) {
@@ -225,68 +229,124 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
           for (int e = 0; e < kTile; ++e)
             if (e >= kvalid) s[e] = -INFINITY;
         }
-        float mt = s[0];
+        float mx[8];
 #pragma unroll
-        for (int e = 1; e < kTile; ++e) mt = fmaxf(mt, s[e]);
-        const float m_new = fmaxf(m, mt);
-        const float alpha = ex2f((m - m_new) * c);
-        const float neg = -m_new * c;
-        float rs = 0.f;
+        for (int g = 0; g < 8; ++g) {
+          float a = fmax3(s[g * 16 + 0], s[g * 16 + 1], s[g * 16 + 2]);
 #pragma unroll
-        for (int e = 0; e < kTile; ++e) {
-          s[e] = ex2f(fmaf(s[e], c, neg));
-          rs += s[e];
+          for (int e = 3; e < 15; e += 2) a = fmax3(a, s[g * 16 + e], s[g * 16 + e + 1]);
+          mx[g] = fmaxf(a, s[g * 16 + 15]);
         }
-        l = fmaf(l, alpha, rs);
-        m = m_new;
-        if (prm.thr != 0) {
+        const float mt = fmaxf(fmax3(mx[0], mx[1], mx[2]), fmaxf(fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        const float m_new = fmaxf(m_run, mt);
+        const bool need = (m_new - m_run) * c > kRescaleThreshold;   // m_run = -inf -> true
+        const float m_ref = need ? m_new : m_run;
+        const float alpha = need ? ex2f((m_run - m_new) * c) : 1.f;
+        const bool rescale_warp = __any_sync(0xffffffffu, need) && j > 0;
+        const float negm = -m_ref * c;
+        const uint64_t neg2 = f2pack(negm, negm);
+        uint64_t acc2[4] = {0, 0, 0, 0};
+        uint32_t pk[kTile / 2];
 #pragma unroll
-          for (int g = 0; g < kTile / 8; ++g) {
+        for (int g = 0; g < kTile / 8; ++g) {          // 8 keys at a time: exp2, sum, dropout, pack
+          float e8[8];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e2 = g * 4 + u;
+            float a, b;
+            f2unpack(ffma2(f2pack(s[2 * e2], s[2 * e2 + 1]), c2, neg2), a, b);
+            if (kPoly > 0 && (e2 & 7) < kPoly) {
+              f2unpack(ex2_poly2(a, b), a, b);
+            } else {
+              a = ex2f(a);
+              b = ex2f(b);
+            }
+            acc2[u] = fadd2(acc2[u], f2pack(a, b));
+            e8[2 * u] = a;
+            e8[2 * u + 1] = b;
+          }
+          if (kDropout) {
             const uint32_t bits = keep_bits8(j * kTile + g * 8, t_glob, it.h, prm.off, prm.k0, prm.k1, prm.thr);
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              if (!((bits >> e) & 1u)) s[g * 8 + e] = 0.f;
+              if (!((bits >> e) & 1u)) e8[e] = 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            pk[g * 4 + u] = kPack ? pack_bf16_int(e8[2 * u], e8[2 * u + 1]) : pack_bf16(e8[2 * u], e8[2 * u + 1]);
+        }
+        float rs;
+        {
+          float a0, a1;
+          f2unpack(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])), a0, a1);
+          rs = a0 + a1;
+        }
+
+        // PV_x(j-1) must have finished reading P and accumulating into O
+        if (j > 0) {
+          mbar_wait(&sm.o_done[x], pv_cnt & 1);
+          ++pv_cnt;
+          tc_fence_after();
+        }
+        if (rescale_warp) {                              // rare: running max grew by > 2^8
+          const uint64_t al2 = f2pack(alpha, alpha);
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            uint32_t o[32];
+            tmem_ld32(t_row + col_o(x) + q * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              float a, b;
+              f2unpack(fmul2(f2pack(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), al2), a, b);
+              o[e] = __float_as_uint(a);
+              o[e + 1] = __float_as_uint(b);
+            }
+            tmem_st32(t_row + col_o(x) + q * 32, o);
           }
         }
-        // P (bf16) -> smem, K-major SW128: chunk g holds keys 8g..8g+7
-        const uint32_t pb = p_it & 1;
-        mbar_wait(&sm.p_empty[pb], ((p_it >> 1) & 1) ^ 1);
-        const uint32_t p_addr = smem_u32(sm.p[pb]);
-#pragma unroll
-        for (int g = 0; g < kTile / 8; ++g) {
-          const uint32_t addr = p_addr + (g >> 3) * (kTile * 128) + sw128_off(r, g & 7);
-          st_shared_v4(addr, pack_bf16(s[g * 8 + 0], s[g * 8 + 1]), pack_bf16(s[g * 8 + 2], s[g * 8 + 3]),
-                       pack_bf16(s[g * 8 + 4], s[g * 8 + 5]), pack_bf16(s[g * 8 + 6], s[g * 8 + 7]));
-        }
-        fence_proxy_async_smem();
+        l = fmaf(l, alpha, rs);
+        m_run = m_ref;
+        tmem_st32(t_row + col_p(x), *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st32(t_row + col_p(x) + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.p_full[pb]);
-        ++p_it;
-        if (j > 0) consume_o(m_tile);
-        m_tile = m;
+        if (lane == 0) mbar_arrive(&sm.p_full[x]);
       }
-      consume_o(m_tile);
-
+      // epilogue: last PV done -> O / l
+      mbar_wait(&sm.o_done[x], pv_cnt & 1);
+      ++pv_cnt;
+      tc_fence_after();
+      uint32_t o0[32], o1[32];
+      tmem_ld32(t_row + col_o(x), o0);
+      tmem_ld32(t_row + col_o(x) + 32, o1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.o_free[x]);
       if (row < it.L) {
         const float inv = prm.rp / l;
         uint4* op = reinterpret_cast<uint4*>(prm.out + ((int64_t)t_glob * H + it.h) * kD);
 #pragma unroll
-        for (int g = 0; g < kD / 8; ++g) {
-          uint4 v;
-          v.x = pack_bf16(acc[g * 8 + 0] * inv, acc[g * 8 + 1] * inv);
-          v.y = pack_bf16(acc[g * 8 + 2] * inv, acc[g * 8 + 3] * inv);
-          v.z = pack_bf16(acc[g * 8 + 4] * inv, acc[g * 8 + 5] * inv);
-          v.w = pack_bf16(acc[g * 8 + 6] * inv, acc[g * 8 + 7] * inv);
-          op[g] = v;
+        for (int g = 0; g < 4; ++g) {
+          op[g] = make_uint4(pack_bf16(__uint_as_float(o0[8 * g]) * inv, __uint_as_float(o0[8 * g + 1]) * inv),
+                             pack_bf16(__uint_as_float(o0[8 * g + 2]) * inv, __uint_as_float(o0[8 * g + 3]) * inv),
+                             pack_bf16(__uint_as_float(o0[8 * g + 4]) * inv, __uint_as_float(o0[8 * g + 5]) * inv),
+                             pack_bf16(__uint_as_float(o0[8 * g + 6]) * inv, __uint_as_float(o0[8 * g + 7]) * inv));
+          op[4 + g] = make_uint4(pack_bf16(__uint_as_float(o1[8 * g]) * inv, __uint_as_float(o1[8 * g + 1]) * inv),
+                                 pack_bf16(__uint_as_float(o1[8 * g + 2]) * inv, __uint_as_float(o1[8 * g + 3]) * inv),
+                                 pack_bf16(__uint_as_float(o1[8 * g + 4]) * inv, __uint_as_float(o1[8 * g + 5]) * inv),
+                                 pack_bf16(__uint_as_float(o1[8 * g + 6]) * inv, __uint_as_float(o1[8 * g + 7]) * inv));
         }
-        prm.lse[(int64_t)it.h * prm.T + t_glob] = m * prm.scale + logf(l);
+        prm.lse[(int64_t)it.h * prm.T + t_glob] = m_run * prm.scale + logf(l);
       }
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -294,17 +354,44 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
 
 }  // namespace fwd
 
+static int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  int v = e ? std::atoi(e) : dflt;
+  return (v < lo || v > hi) ? dflt : v;
+}
+
+template <int P, int K>
+static void (*pick_fwd(bool drop))(CUtensorMap, fwd::Params) {
+  return drop ? fwd::fmha_fwd_kernel<P, K, true> : fwd::fmha_fwd_kernel<P, K, false>;
+}
+
 ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out, float* lse,
                          void* ws, cudaStream_t s) {
-  UB_CHECK_CUDA(cudaFuncSetAttribute(fwd::fmha_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)fwd::kSmemBytes));
+  // tuning knobs (measured defaults; env overrides are for sweeps)
+  static const int poly = env_int("UB_FWD_POLY", 2, 0, 4);
+  static const int pack = env_int("UB_FWD_PACK", 0, 0, 1);
+  const bool drop = p.p_dropout > 0.f;
+  void (*kern)(CUtensorMap, fwd::Params);
+  switch (poly * 2 + pack) {
+    case 0: kern = pick_fwd<0, 0>(drop); break;
+    case 1: kern = pick_fwd<0, 1>(drop); break;
+    case 2: kern = pick_fwd<1, 0>(drop); break;
+    case 3: kern = pick_fwd<1, 1>(drop); break;
+    case 4: kern = pick_fwd<2, 0>(drop); break;
+    case 5: kern = pick_fwd<2, 1>(drop); break;
+    case 6: kern = pick_fwd<3, 0>(drop); break;
+    case 7: kern = pick_fwd<3, 1>(drop); break;
+    case 8: kern = pick_fwd<4, 0>(drop); break;
+    default: kern = pick_fwd<4, 1>(drop); break;
+  }
+  UB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::kSmemBytes));
   CUtensorMap tmap;
   ub_status st = make_tmap_bf16(&tmap, qkv, (uint64_t)3 * p.heads * fwd::kD, (uint64_t)p.T,
                                 (uint64_t)3 * p.heads * fwd::kD * 2);
   if (st != UB_OK) return st;
   FmhaPlanView v = fmha_plan_view(ws, p.B);
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
-  if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, v, s)) != UB_OK) return st;
+  if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 2, v, s)) != UB_OK) return st;
 
   fwd::Params prm{};
   prm.cu = d_cu;
@@ -325,12 +412,11 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // upper bound on items: H * (B + T/128); one CTA per SM, persistent
-  const int64_t max_items = (int64_t)p.heads * (p.B + p.T / kTile + 1);
+  const int64_t max_items = (int64_t)p.heads * (p.B + p.T / (2 * kTile) + 1);
   const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfFwd, 0, s);
-  fwd::fmha_fwd_kernel<<<grid, fwd::kThreads, fwd::kSmemBytes, s>>>(tmap, prm);
+  kern<<<grid, fwd::kThreads, fwd::kSmemBytes, s>>>(tmap, prm);
   UB_CHECK_LAUNCH();
   prof_record(kProfFwd, 1, s);
   return UB_OK;

@@ -7,9 +7,10 @@
 // a flat item list that one persistent launch walks.  cu_seqlens stays on the device:
 // no host sync, no D2H of the lengths.
 //
-// Work item = (sequence, head, 128-row tile).  Forward: tile = query tile, cost = #key
-// tiles.  Backward: tile = key tile, cost = #query tiles.  Both costs equal the
-// sequence's tile count, so one plan serves both directions.
+// Work item = (sequence, head, group of `tiles_per_item` 128-row tiles).  Forward: pairs
+// of query tiles (the two softmax warpgroups share K/V), cost = 2 x #key tiles.  Backward:
+// one key tile, cost = #query tiles.  Costs grow with the sequence's tile count, so
+// bucketing by tile count orders items longest-first in both directions.
 #include "ub_internal.h"
 
 namespace ub {
@@ -30,7 +31,7 @@ FmhaPlanView fmha_plan_view(void* ws, int32_t B) {
 }
 
 __global__ void __launch_bounds__(32) fmha_plan_kernel(const int32_t* __restrict__ cu, int32_t B, int32_t H,
-                                                       int32_t max_tiles, FmhaPlanView v) {
+                                                       int32_t max_tiles, int32_t tiles_per_item, FmhaPlanView v) {
   const uint32_t lane = threadIdx.x;
   if (lane < 4) v.counters[lane] = 0;
   const uint32_t lt = (1u << lane) - 1u;
@@ -59,7 +60,8 @@ __global__ void __launch_bounds__(32) fmha_plan_kernel(const int32_t* __restrict
     if (k < B) {
       const int32_t b = v.seq_order[k];
       const int32_t L = cu[b + 1] - cu[b];
-      items = (L > 0 ? (L + kTile - 1) / kTile : 0) * H;
+      const int32_t nt = L > 0 ? (L + kTile - 1) / kTile : 0;
+      items = (nt + tiles_per_item - 1) / tiles_per_item * H;
     }
     int32_t incl = items;
 #pragma unroll
@@ -73,9 +75,9 @@ __global__ void __launch_bounds__(32) fmha_plan_kernel(const int32_t* __restrict
   if (lane == 0) v.item_prefix[B] = running;
 }
 
-ub_status launch_fmha_plan(const int32_t* d_cu, int32_t B, int32_t H, int32_t max_tiles, FmhaPlanView v,
-                           cudaStream_t s) {
-  fmha_plan_kernel<<<1, 32, 0, s>>>(d_cu, B, H, max_tiles, v);
+ub_status launch_fmha_plan(const int32_t* d_cu, int32_t B, int32_t H, int32_t max_tiles, int32_t tiles_per_item,
+                           FmhaPlanView v, cudaStream_t s) {
+  fmha_plan_kernel<<<1, 32, 0, s>>>(d_cu, B, H, max_tiles, tiles_per_item, v);
   UB_CHECK_LAUNCH();
   return UB_OK;
 }

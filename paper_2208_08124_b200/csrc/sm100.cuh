@@ -47,6 +47,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_
       :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// 2-D tiled reduce-add (fp32 add at L2) of an smem box into the tensor, bulk-group tracked.
+__device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* src, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];"
+      :: "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(src)), "r"(c0), "r"(c1) : "memory");
+}
+// named barrier over `count` threads (ids 1..15; 0 is __syncthreads)
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(count) : "memory");
+}
 // 1-D bulk reduce-add of fp32 from smem into global (dst must be 16-B aligned, bytes % 16 == 0).
 __device__ __forceinline__ void bulk_reduce_add_f32(float* gdst, const void* ssrc, uint32_t bytes) {
   asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;"
@@ -80,6 +90,16 @@ __device__ __forceinline__ void umma_bf16_ss(uint32_t d_tmem, uint64_t adesc, ui
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
       :: "r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T: A (M x K bf16) read from TMEM, lane = row, K packed
+// two bf16 per 32-bit column (lower K index in the low half).
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      :: "r"(d_tmem), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
 // mbarrier arrives once all previously issued tcgen05 async ops of this thread complete.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -99,6 +119,95 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// 32 lanes x 32 columns store (thread t -> lane base + t).
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+         "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+         "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+         "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Per-warpgroup register reallocation (all 4 warps of the warpgroup must execute it).
+template <uint32_t N> __device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(N)); }
+template <uint32_t N> __device__ __forceinline__ void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(N)); }
+
+// ---------------------------------------------------------------- packed fp32x2 / 3-input max
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// 2^x for a pair of values on the FMA pipe only (no XU/MUFU op): round-to-nearest split
+// x = n + f via the 1.5*2^23 magic add, f in [-0.5, 0.5], degree-3 minimax polynomial for
+// 2^f (max rel. error 1.0e-4 < bf16 half-ulp), exponent add by integer multiply-add.
+// x is clamped at -127 so masked (-inf) and underflowing entries give ~0.
+__device__ __forceinline__ uint64_t ex2_poly2(float xa, float xb) {
+  const float magic = 12582912.0f;
+  xa = fmaxf(xa, -127.f);
+  xb = fmaxf(xb, -127.f);
+  const uint64_t x2 = f2pack(xa, xb);
+  const uint64_t t2 = fadd2(x2, f2pack(magic, magic));
+  const uint64_t n2 = fadd2(t2, f2pack(-magic, -magic));
+  const uint64_t f2 = fadd2(x2, n2 ^ 0x8000000080000000ull);       // x - n
+  uint64_t p2 = ffma2(f2, f2pack(0.05500874f, 0.05500874f), f2pack(0.24221049f, 0.24221049f));
+  p2 = ffma2(p2, f2, f2pack(0.69328298f, 0.69328298f));
+  p2 = ffma2(p2, f2, f2pack(1.0f, 1.0f));
+  const uint32_t tlo = (uint32_t)t2, thi = (uint32_t)(t2 >> 32);
+  uint32_t plo = (uint32_t)p2, phi = (uint32_t)(p2 >> 32);
+  asm("mad.lo.u32 %0, %1, 8388608, %0;" : "+r"(plo) : "r"(tlo));
+  asm("mad.lo.u32 %0, %1, 8388608, %0;" : "+r"(phi) : "r"(thi));
+  return ((uint64_t)phi << 32) | plo;
+}
+// bf16x2 pack with round-half-away on the integer pipes (keeps the XU pipe, which also
+// executes MUFU.EX2, free): add 0x8000 to each fp32 pattern, take the high halves.
+__device__ __forceinline__ uint32_t pack_bf16_int(float lo, float hi) {
+  uint32_t a = __float_as_uint(lo), b = __float_as_uint(hi), r;
+  asm("mad.lo.u32 %0, %0, 1, 32768;" : "+r"(a));
+  asm("mad.lo.u32 %0, %0, 1, 32768;" : "+r"(b));
+  asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// 2^x on the FMA pipe (x <= 0): Cody-Waite split x = j + f, f in [0,1), degree-3 minimax
+// polynomial for 2^f (max rel. error 8.6e-5, below bf16 resolution of P), exponent add.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float j = floorf(x);
+  const float f = x - j;
+  float p = fmaf(f, 0.07706573f, 0.22764572f);
+  p = fmaf(p, f, 0.69511703f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (static_cast<int>(j) << 23));
+}
 
 // ---------------------------------------------------------------- descriptors
 // Shared-memory matrix descriptor (sm_100 "version 1"), SWIZZLE_128B (layout type 2).

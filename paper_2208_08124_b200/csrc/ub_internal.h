@@ -53,7 +53,7 @@ struct FmhaPlanView {   // device views into the workspace, filled by the plan k
 
 size_t fmha_plan_bytes(int32_t B);
 FmhaPlanView fmha_plan_view(void* ws, int32_t B);
-ub_status launch_fmha_plan(const int32_t* d_cu, int32_t B, int32_t H, int32_t max_tiles,
+ub_status launch_fmha_plan(const int32_t* d_cu, int32_t B, int32_t H, int32_t max_tiles, int32_t tiles_per_item,
                            FmhaPlanView v, cudaStream_t s);
 
 ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out,
