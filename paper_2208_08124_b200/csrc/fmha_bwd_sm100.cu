@@ -16,8 +16,8 @@
 // CTA = 10 warps (1 per SM):
 //   warps 0-7  two compute warpgroups: thread r of warpgroup x owns key row r and query
 //              columns [64x, 64x+64) of S^T / dP^T; it also stages its half of dQ
-//   warp 8     TMA producer (K, V per item, double-buffered; Q, dO per query tile, 2 stages)
-//              + the LSE / Delta vectors of the query tile into smem (all 32 lanes)
+//   warp 8     producer: K, V per item (double-buffered) and Q, dO per query tile (2 stages)
+//              by TMA; the tile's LSE / Delta vectors by the 32 lanes into smem
 //   warp 9     TMEM allocator, then MMA issuer (one thread)
 // TMEM columns: S^T 0..127, dP^T 128..255, P~^T 256..319 (bf16 pairs), dS^T 320..383
 // (bf16 pairs; dQ_i = dS K is written over it after dK_i has read it -- tcgen05.mma ops of
@@ -46,12 +46,13 @@ struct Smem {
   uint8_t dO[2][kTileBytes];
   uint8_t ds[kPBytes];              // dS^T [key][query], 2 x 64-query SW128 regions
   uint8_t dq[2][kTile * 128];       // dQ staging per warpgroup: [128 rows][32 fp32] SW128
-  float lse2[2][kTile];             // LSE * log2(e) per query row (+inf past the sequence)
+  float lse[2][kTile];              // LSE of the query tile's rows (natural log)
   float delta[2][kTile];
   uint64_t kv_full[2], kv_empty[2];
   uint64_t qdo_full[2], qdo_empty[2];
   uint64_t s_full, s_free, pds_full, pds_empty, dkv_full, dkv_free;
   uint32_t tmem_base;
+  PlanSmem plan;
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
 
@@ -90,7 +91,8 @@ __device__ __forceinline__ uint32_t keep8_cols(uint32_t key_grp_j0, uint32_t t_q
 template <bool kDropout>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_constant__ CUtensorMap tmap_do,
-                const __grid_constant__ CUtensorMap tmap_dq, const Params prm) {
+                const __grid_constant__ CUtensorMap tmap_dq, const __grid_constant__ CUtensorMap tmap_lse,
+                const __grid_constant__ CUtensorMap tmap_delta, const Params prm) {
   extern __shared__ uint8_t smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t warp = warp_id_sync();
@@ -100,6 +102,8 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     tma_prefetch_desc(&tmap_qkv);
     tma_prefetch_desc(&tmap_do);
     tma_prefetch_desc(&tmap_dq);
+    tma_prefetch_desc(&tmap_lse);
+    tma_prefetch_desc(&tmap_delta);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], 1);
@@ -114,6 +118,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     mbar_init(&sm.dkv_free, 8);
     fence_mbar_init();
   }
+  load_plan_smem(sm.plan, prm.plan, prm.cu, prm.B);
   if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
@@ -125,7 +130,8 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     // ------------------------------------------------------------ producer
     uint32_t items = 0, qit = 0;
     WorkItem it;
-    for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+    for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it);
+         w += gridDim.x, ++items) {
       const uint32_t kvs = items & 1;
       if (lane == 0) {
         mbar_wait(&sm.kv_empty[kvs], ((items >> 1) & 1) ^ 1);
@@ -136,19 +142,28 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       }
       for (int32_t i = 0; i < it.nt; ++i, ++qit) {
         const uint32_t st = qit & 1;
+        const int32_t q0 = it.c0 + i * kTile;
+        // LSE / Delta loads are issued before the stage wait so their latency hides behind it
+        float lv[4], dv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int32_t k = (int32_t)lane + 32 * u;
+          const bool ok = i * kTile + k < it.L;
+          const int64_t idx = (int64_t)it.h * prm.T + q0 + k;
+          lv[u] = ok ? __ldg(prm.lse + idx) : 0.f;
+          dv[u] = ok ? __ldg(prm.delta + idx) : 0.f;
+        }
         mbar_wait(&sm.qdo_empty[st], ((qit >> 1) & 1) ^ 1);
-        for (int k = (int)lane; k < kTile; k += 32) {
-          const int32_t row = i * kTile + k;
-          const bool ok = row < it.L;
-          const int64_t t = (int64_t)it.c0 + row;
-          sm.lse2[st][k] = ok ? prm.lse[(int64_t)it.h * prm.T + t] * 1.4426950408889634f : INFINITY;
-          sm.delta[st][k] = ok ? prm.delta[(int64_t)it.h * prm.T + t] : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          sm.lse[st][lane + 32 * u] = lv[u];
+          sm.delta[st][lane + 32 * u] = dv[u];
         }
         __syncwarp();
         if (lane == 0) {
           mbar_expect_tx(&sm.qdo_full[st], 2 * kTileBytes);
-          tma_load_2d(sm.q[st], &tmap_qkv, &sm.qdo_full[st], it.h * kD, it.c0 + i * kTile);
-          tma_load_2d(sm.dO[st], &tmap_do, &sm.qdo_full[st], it.h * kD, it.c0 + i * kTile);
+          tma_load_2d(sm.q[st], &tmap_qkv, &sm.qdo_full[st], it.h * kD, q0);
+          tma_load_2d(sm.dO[st], &tmap_do, &sm.qdo_full[st], it.h * kD, q0);
         }
         __syncwarp();
       }
@@ -159,7 +174,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       uint32_t items = 0, qit = 0, s_cnt = 0, g_cnt = 0;
       const uint32_t ds_addr = smem_u32(sm.ds);
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+      for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
         const uint32_t kvs = items & 1;
         const uint32_t k_addr = smem_u32(sm.k[kvs]), v_addr = smem_u32(sm.v[kvs]);
         mbar_wait(&sm.kv_full[kvs], (items >> 1) & 1);
@@ -215,6 +230,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     const uint32_t t_row = tmem + (((warp & 3) * 32) << 16);
     const float c = prm.scale_log2;
     const uint64_t c2 = f2pack(c, c);
+    const uint64_t nl2e2 = f2pack(-1.4426950408889634f, -1.4426950408889634f);
     const uint32_t ds_addr = smem_u32(sm.ds) + x * (kTile * 128);
     const uint32_t dq_addr = smem_u32(sm.dq[x]);
     uint32_t s_cnt = 0, g_cnt = 0, qit = 0, items = 0;
@@ -240,12 +256,13 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       }
     };
 
-    for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+    for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
       const int32_t key = it.tile * kTile + (int32_t)r;
       const bool key_ok = key < it.L;
       const uint32_t grp_j0 = (uint32_t)(it.tile * kTile) + (warp & 3) * 32 + (lane & ~7u);
       for (int32_t i = 0; i < it.nt; ++i, ++qit) {
         const uint32_t st = qit & 1;
+        const int32_t qvalid = it.L - i * kTile;          // query rows of this tile inside the sequence
         mbar_wait(&sm.qdo_full[st], (qit >> 1) & 1);     // LSE / Delta of this query tile
         mbar_wait(&sm.s_full, s_cnt & 1);
         tc_fence_after();
@@ -273,13 +290,13 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           }
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse2[st][q0 + e]);
+            const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse[st][q0 + e]);
             const float2 dl = *reinterpret_cast<const float2*>(&sm.delta[st][q0 + e]);
             float pa, pb;
             f2unpack(ffma2(f2pack(__uint_as_float(sr[ch][e]), __uint_as_float(sr[ch][e + 1])), c2,
-                           f2pack(-l2.x, -l2.y)), pa, pb);
-            pa = key_ok ? ex2f(pa) : 0.f;
-            pb = key_ok ? ex2f(pb) : 0.f;
+                           fmul2(f2pack(l2.x, l2.y), nl2e2)), pa, pb);
+            pa = (key_ok && q0 + e < qvalid) ? ex2f(pa) : 0.f;
+            pb = (key_ok && q0 + e + 1 < qvalid) ? ex2f(pb) : 0.f;
             float dpa = __uint_as_float(dr[ch][e]), dpb = __uint_as_float(dr[ch][e + 1]);
             float qa = pa, qb = pb;
             if (kDropout) {
@@ -419,7 +436,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   char* extra = base + align_up(fmha_plan_bytes(p.B), 256);
   float* delta = reinterpret_cast<float*>(extra);
   float* dq_acc = reinterpret_cast<float*>(extra + align_up((size_t)p.T * p.heads * 4, 256));
-  CUtensorMap tq, tdo, tdq;
+  CUtensorMap tq, tdo, tdq, tlse, tdl;
   ub_status st = make_tmap_bf16(&tq, qkv, (uint64_t)3 * p.heads * bwd::kD, (uint64_t)p.T,
                                 (uint64_t)3 * p.heads * bwd::kD * 2);
   if (st != UB_OK) return st;
@@ -427,6 +444,8 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
       UB_OK)
     return st;
   if ((st = make_tmap_f32(&tdq, dq_acc, bwd::kD, (uint64_t)p.T * p.heads, bwd::kD * 4, 32, kTile)) != UB_OK) return st;
+  if ((st = make_tmap_f32_1d(&tlse, lse, (uint64_t)p.T * p.heads, kTile)) != UB_OK) return st;
+  if ((st = make_tmap_f32_1d(&tdl, delta, (uint64_t)p.T * p.heads, kTile)) != UB_OK) return st;
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
   if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 1, v, s)) != UB_OK) return st;
   const int64_t rows = p.T * p.heads;
@@ -459,7 +478,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfBwd, 0, s);
-  kern<<<grid, bwd::kThreads, bwd::kSmemBytes, s>>>(tq, tdo, tdq, prm);
+  kern<<<grid, bwd::kThreads, bwd::kSmemBytes, s>>>(tq, tdo, tdq, tlse, tdl, prm);
   UB_CHECK_LAUNCH();
   prof_record(kProfBwd, 1, s);
   const int64_t n = rows * (bwd::kD / 8);

@@ -35,6 +35,53 @@ __device__ __forceinline__ bool decode_item(int32_t w, const FmhaPlanView& v, co
   return true;
 }
 
+// Shared-memory copy of the plan (one per CTA, loaded once at kernel start) so that work
+// decoding costs a few shared loads instead of a chain of dependent L2 loads per item.
+constexpr int kPlanCap = 1024;   // sequences; larger batches decode from global memory
+struct PlanSmem {
+  int32_t prefix[kPlanCap + 1];  // item prefix along the bucketed order
+  int32_t seq[kPlanCap];         // sequence id
+  int32_t c0[kPlanCap];          // cu_seqlens[seq]
+  int32_t len[kPlanCap];         // length of seq
+};
+
+__device__ __forceinline__ void load_plan_smem(PlanSmem& ps, const FmhaPlanView& v, const int32_t* __restrict__ cu,
+                                               int32_t B) {
+  if (B > kPlanCap) return;
+  for (int k = threadIdx.x; k <= B; k += blockDim.x) {
+    ps.prefix[k] = v.item_prefix[k];
+    if (k < B) {
+      const int32_t b = v.seq_order[k];
+      const int32_t a = cu[b];
+      ps.seq[k] = b;
+      ps.c0[k] = a;
+      ps.len[k] = cu[b + 1] - a;
+    }
+  }
+}
+
+__device__ __forceinline__ bool decode_item_smem(int32_t w, const PlanSmem& ps, const FmhaPlanView& v,
+                                                 const int32_t* __restrict__ cu, int32_t B, int32_t H,
+                                                 int32_t tiles_per_item, WorkItem& it) {
+  if (B > kPlanCap) return decode_item(w, v, cu, B, H, tiles_per_item, it);
+  if (w >= ps.prefix[B]) return false;
+  int32_t lo = 0, hi = B;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    if (ps.prefix[mid] <= w) lo = mid; else hi = mid - 1;
+  }
+  it.b = ps.seq[lo];
+  const int32_t local = w - ps.prefix[lo];
+  it.c0 = ps.c0[lo];
+  it.L = ps.len[lo];
+  it.nt = (it.L + kTile - 1) / kTile;
+  const int32_t ngroups = (it.nt + tiles_per_item - 1) / tiles_per_item;
+  it.h = local / ngroups;
+  it.tile = (local - it.h * ngroups) * tiles_per_item;
+  it.ntile = min(tiles_per_item, it.nt - it.tile);
+  return true;
+}
+
 // Dropout keep bits for 8 consecutive keys j0..j0+7 (j0 % 8 == 0) of packed row t (R5):
 // bit e set <=> key j0+e kept.
 __device__ __forceinline__ uint32_t keep_bits8(uint32_t j0, uint32_t t, uint32_t h, uint32_t off, uint32_t k0,
@@ -56,6 +103,8 @@ ub_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint
                          uint32_t box_cols = 64, uint32_t box_rows = 128);
 // Host: 2-D fp32 tensor map (row-major [rows, cols]), box {box_cols, box_rows}, 128-B swizzle
 // (box_cols * 4 must be 128).
+// Host: 1-D fp32 tensor map over n elements, box of `box` elements (no swizzle).
+ub_status make_tmap_f32_1d(CUtensorMap* map, const void* base, uint64_t n, uint32_t box);
 ub_status make_tmap_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
                         uint32_t box_cols, uint32_t box_rows);
 

@@ -46,6 +46,7 @@ struct Smem {
   uint64_t k_full[kStages], v_full[kStages], kv_empty[kStages];
   uint64_t s_full[2], s_free[2], p_full[2], o_done[2], o_free[2];   // per warpgroup
   uint32_t tmem_base;
+  PlanSmem plan;
 };
 constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
 
@@ -97,6 +98,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
     }
     fence_mbar_init();
   }
+  load_plan_smem(sm.plan, prm.plan, prm.cu, prm.B);
   if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
@@ -111,7 +113,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
     if (lane == 0) {
       uint32_t items = 0, kv_it = 0;
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
+      for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
         const uint32_t slot = items & 1;
         mbar_wait(&sm.q_empty[slot], ((items >> 1) & 1) ^ 1);
         mbar_expect_tx(&sm.q_full[slot], kTileBytes * it.ntile);
@@ -133,7 +135,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
       uint32_t items = 0, kv_it = 0;
       uint32_t s_cnt[2] = {0, 0}, p_cnt[2] = {0, 0}, it_cnt[2] = {0, 0};
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
+      for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
         const uint32_t slot = items & 1;
         const int nx = it.ntile;
         mbar_wait(&sm.q_full[slot], (items >> 1) & 1);
@@ -199,7 +201,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
     const uint64_t c2 = f2pack(c, c);
     uint32_t s_cnt = 0, pv_cnt = 0;
     WorkItem it;
-    for (int32_t w = blockIdx.x; decode_item(w, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x) {
+    for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x) {
       if (x >= it.ntile) continue;
       const int32_t row = (it.tile + x) * kTile + (int32_t)r;
       const uint32_t t_glob = (uint32_t)(it.c0 + row);

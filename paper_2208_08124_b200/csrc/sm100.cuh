@@ -47,6 +47,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_
       :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// 1-D tiled load (tensor map of rank 1): box of the map's size lands at dst.
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* tmap, uint64_t* bar, int32_t c0) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(smem_u32(bar))
+      : "memory");
+}
 // 2-D tiled reduce-add (fp32 add at L2) of an smem box into the tensor, bulk-group tracked.
 __device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* src, int32_t c0, int32_t c1) {
   asm volatile(

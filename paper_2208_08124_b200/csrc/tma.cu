@@ -50,4 +50,18 @@ ub_status make_tmap_f32(CUtensorMap* map, const void* base, uint64_t cols, uint6
   return UB_OK;
 }
 
+ub_status make_tmap_f32_1d(CUtensorMap* map, const void* base, uint64_t n, uint32_t box) {
+  auto enc = get_encode();
+  UB_REQUIRE(enc != nullptr, UB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[1] = {n};
+  cuuint64_t strides[1] = {n * 4};
+  cuuint32_t boxd[1] = {box};
+  cuuint32_t estr[1] = {1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 1, const_cast<void*>(base), dims, strides, boxd, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  UB_REQUIRE(r == CUDA_SUCCESS, UB_ERR_CUDA, "cuTensorMapEncodeTiled (f32 1-D) failed (%d)", (int)r);
+  return UB_OK;
+}
+
 }  // namespace ub
