@@ -48,7 +48,7 @@ struct Smem {
   uint32_t tmem_base;
   PlanSmem plan;
 };
-constexpr size_t kSmemBytes = sizeof(Smem) + 1024;
+constexpr size_t kSmemBytes = sizeof(Smem);
 
 struct Params {
   const int32_t* cu;
@@ -75,8 +75,12 @@ __host__ __device__ constexpr uint32_t col_o(int x) { return 256u * x + 192u; }
 template <int kPoly, int kPack, bool kDropout>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // Taken straight from the __shared__ array so that every access compiles to LDS/STS (a
+  // generic pointer would turn them into long-latency generic loads); the dynamic smem
+  // window starts 1024-B aligned (checked), as the 128-B swizzle atoms require.
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
 
