@@ -43,14 +43,19 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
+    """trace=True builds libub_trace.so with -DUB_TRACE (debug timelines; not the product)."""
+    build_dir = BUILD + ("_trace" if trace else "")
+    lib = LIB.replace("libub.so", "libub_trace.so") if trace else LIB
+    os.makedirs(build_dir, exist_ok=True)
     nccl, flags = _flags()
+    if trace:
+        flags = flags + ["-DUB_TRACE"]
     hdrs = _headers()
     jobs = []
     objs = []
     for src in _sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + hdrs):
             jobs.append([NVCC] + flags + ["-c", src, "-o", obj])
@@ -65,15 +70,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
+    if force or jobs or _stale(lib, objs):
         nccl_lib = os.path.join(nccl, "lib")
         # export only the C ABI (ub_*): visibility=hidden + explicit default in ub.h users
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + [
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + [
             "-L" + nccl_lib, "-l:libnccl.so.2", "-lcudart",
             "-Xlinker", "-rpath," + nccl_lib, "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")]
         run(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))

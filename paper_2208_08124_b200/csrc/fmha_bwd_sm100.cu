@@ -24,14 +24,26 @@
 // one thread execute in issue order), dV 384..447, dK 448..511.
 // The MMA issues S_{i+1}, dP_{i+1} as soon as the compute warps have loaded S_i, dP_i, so
 // the exp/dS phase of tile i overlaps the tensor work of tile i+1.
-// dQ_i leaves through smem staging (128-B swizzle) and cp.reduce.async.bulk.tensor add into
-// an fp32 [H*T, 64] accumulator: one TMA op per 32 columns instead of 8192 atomics.
+// dQ_i leaves through per-warp smem staging (128-B swizzle) and cp.reduce.async.bulk.tensor
+// add into an fp32 [H*T, 64] accumulator (one TMA op per warp instead of 8192 atomics);
+// dK / dV of whole warps leave by TMA store from the same staging (64-B swizzle).
 #include <cmath>
 
 #include "fmha_common.cuh"
 
 namespace ub {
 namespace bwd {
+
+#ifdef UB_TRACE
+__device__ uint64_t g_trace[10 * 1024];
+#define TR(ev)                                                                                          \
+  do {                                                                                                  \
+    if (blockIdx.x == 0 && lane == 0 && tr_n < 1024)                                                    \
+      g_trace[warp * 1024 + tr_n++] = ((uint64_t)(ev) << 48) | ((uint64_t)clock64() & 0xFFFFFFFFFFFFull); \
+  } while (0)
+#else
+#define TR(ev) do {} while (0)
+#endif
 
 constexpr int kD = 64;
 constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
@@ -88,11 +100,11 @@ __device__ __forceinline__ uint32_t keep8_cols(uint32_t key_grp_j0, uint32_t t_q
   return bits;
 }
 
-template <bool kDropout>
+template <bool kDropout, bool kBigB>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_constant__ CUtensorMap tmap_do,
-                const __grid_constant__ CUtensorMap tmap_dq, const __grid_constant__ CUtensorMap tmap_lse,
-                const __grid_constant__ CUtensorMap tmap_delta, const Params prm) {
+                const __grid_constant__ CUtensorMap tmap_dq, const __grid_constant__ CUtensorMap tmap_dkv,
+                const Params prm) {
   // Taken straight from the __shared__ array so that every access compiles to LDS/STS (a
   // generic pointer would turn them into long-latency generic loads); the dynamic smem
   // window starts 1024-B aligned (checked), as the 128-B swizzle atoms require.
@@ -101,13 +113,14 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
+  uint32_t tr_n = 0;
+  (void)tr_n;
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
     tma_prefetch_desc(&tmap_do);
     tma_prefetch_desc(&tmap_dq);
-    tma_prefetch_desc(&tmap_lse);
-    tma_prefetch_desc(&tmap_delta);
+    tma_prefetch_desc(&tmap_dkv);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], 1);
@@ -122,7 +135,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     mbar_init(&sm.dkv_free, 8);
     fence_mbar_init();
   }
-  load_plan_smem(sm.plan, prm.plan, prm.cu, prm.B);
+  load_plan_smem<kBigB>(sm.plan, prm.plan, prm.cu, prm.B);
   if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
@@ -134,11 +147,13 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     // ------------------------------------------------------------ producer
     uint32_t items = 0, qit = 0;
     WorkItem it;
-    for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it);
+    for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it);
          w += gridDim.x, ++items) {
       const uint32_t kvs = items & 1;
       if (lane == 0) {
+        TR(20);
         mbar_wait(&sm.kv_empty[kvs], ((items >> 1) & 1) ^ 1);
+        TR(21);
         mbar_expect_tx(&sm.kv_full[kvs], 2 * kTileBytes);
         const int32_t krow = it.c0 + it.tile * kTile;
         tma_load_2d(sm.k[kvs], &tmap_qkv, &sm.kv_full[kvs], (H + it.h) * kD, krow);
@@ -157,7 +172,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           lv[u] = ok ? __ldg(prm.lse + idx) : 0.f;
           dv[u] = ok ? __ldg(prm.delta + idx) : 0.f;
         }
+        TR(22);
         mbar_wait(&sm.qdo_empty[st], ((qit >> 1) & 1) ^ 1);
+        TR(23);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           sm.lse[st][lane + 32 * u] = lv[u];
@@ -168,6 +185,10 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           mbar_expect_tx(&sm.qdo_full[st], 2 * kTileBytes);
           tma_load_2d(sm.q[st], &tmap_qkv, &sm.qdo_full[st], it.h * kD, q0);
           tma_load_2d(sm.dO[st], &tmap_do, &sm.qdo_full[st], it.h * kD, q0);
+          if (i + 1 < it.nt) {                       // warm L2 for the next stage's tile
+            tma_prefetch_2d(&tmap_qkv, it.h * kD, q0 + kTile);
+            tma_prefetch_2d(&tmap_do, it.h * kD, q0 + kTile);
+          }
         }
         __syncwarp();
       }
@@ -178,13 +199,16 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       uint32_t items = 0, qit = 0, s_cnt = 0, g_cnt = 0;
       const uint32_t ds_addr = smem_u32(sm.ds);
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+      for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
         const uint32_t kvs = items & 1;
         const uint32_t k_addr = smem_u32(sm.k[kvs]), v_addr = smem_u32(sm.v[kvs]);
+        TR(16);
         mbar_wait(&sm.kv_full[kvs], (items >> 1) & 1);
+        TR(17);
         auto grads = [&](uint32_t st, bool first) {
           mbar_wait(&sm.pds_full, g_cnt & 1);
           if (first) mbar_wait(&sm.dkv_free, (items & 1) ^ 1);
+          TR(12);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
@@ -195,19 +219,21 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           for (uint32_t k = 0; k < kTile / 16; ++k)
             umma_bf16_ts(tmem + kColDK, tmem + kColDS + k * 8, sdesc_sw128(q_addr + k * 2048, 8192, 1024), kIdescTS,
                          (first && k == 0) ? 0u : 1u);
+          umma_commit(&sm.qdo_empty[st]);                // Q_i / dO_i no longer needed
 #pragma unroll
           for (uint32_t k = 0; k < kTile / 16; ++k)        // K = key rows, 16 per MMA
             umma_bf16_ss(tmem + kColDQ, sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024),
                          sdesc_sw128(k_addr + k * 2048, 8192, 1024), kIdescQ, k > 0);
           umma_commit(&sm.pds_empty);
-          umma_commit(&sm.qdo_empty[st]);
           ++g_cnt;
         };
         uint32_t prev_st = 0;
         for (int32_t i = 0; i < it.nt; ++i, ++qit) {
           const uint32_t st = qit & 1;
           mbar_wait(&sm.qdo_full[st], (qit >> 1) & 1);
+          TR(18);
           mbar_wait(&sm.s_free, (s_cnt & 1) ^ 1);
+          TR(10);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
 #pragma unroll
@@ -242,33 +268,43 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     int32_t prev_row0 = 0;                                  // dQ accumulator row of the pending tile
     WorkItem it;
 
+    // per-warp staging slice (32 rows x 128 B) of the warpgroup's dQ buffer; every warp
+    // moves its own rows, so no cross-warp barrier is needed
+    const uint32_t lr = r & 31u;
+    uint8_t* stage = sm.dq[x] + (warp & 3) * 4096;
+    const uint32_t stage_addr = smem_u32(stage);
+    auto stage_free = [&]() {                               // this warp's previous bulk op read it
+      if (lane == 0) bulk_wait_group_read0();
+      __syncwarp();
+    };
     auto dq_epilogue = [&](int32_t row0) {
       // pds_empty (waited by the caller) means dQ of the previous tile sits in TMEM
       uint32_t d[32];
       tmem_ld32(t_row + kColDQ + x * 32, d);
       tmem_ld_wait();
-      if (threadIdx.x == 128u * x) bulk_wait_group_read0();   // staging buffer free again
-      named_bar_sync(1 + x, 128);
+      stage_free();
 #pragma unroll
       for (int g = 0; g < 8; ++g)
-        st_shared_v4(dq_addr + sw128_off(r, g), d[4 * g], d[4 * g + 1], d[4 * g + 2], d[4 * g + 3]);
+        st_shared_v4(stage_addr + sw128_off(lr, g), d[4 * g], d[4 * g + 1], d[4 * g + 2], d[4 * g + 3]);
       fence_proxy_async_smem();
-      named_bar_sync(1 + x, 128);
-      if (threadIdx.x == 128u * x) {
-        tma_reduce_add_2d(&tmap_dq, sm.dq[x], (int32_t)(x * 32), row0);
+      __syncwarp();
+      if (lane == 0) {
+        tma_reduce_add_2d(&tmap_dq, stage, (int32_t)(x * 32), row0 + (int32_t)(warp & 3) * 32);
         bulk_commit_group();
       }
     };
 
-    for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+    for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
       const int32_t key = it.tile * kTile + (int32_t)r;
       const bool key_ok = key < it.L;
       const uint32_t grp_j0 = (uint32_t)(it.tile * kTile) + (warp & 3) * 32 + (lane & ~7u);
       for (int32_t i = 0; i < it.nt; ++i, ++qit) {
         const uint32_t st = qit & 1;
         const int32_t qvalid = it.L - i * kTile;          // query rows of this tile inside the sequence
+        TR(1);
         mbar_wait(&sm.qdo_full[st], (qit >> 1) & 1);     // LSE / Delta of this query tile
         mbar_wait(&sm.s_full, s_cnt & 1);
+        TR(2);
         tc_fence_after();
         uint32_t sr[2][32], dr[2][32];
         tmem_ld32(t_row + kColS + x * 64, sr[0]);
@@ -280,6 +316,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.s_free);
         ++s_cnt;
+        TR(3);
 
         uint32_t pp[32], pd[32];
 #pragma unroll
@@ -317,9 +354,12 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           }
         }
         // grads of the previous tile done: P~^T / dS^T TMEM and dS smem are free, dQ ready
+        TR(4);
         mbar_wait(&sm.pds_empty, (g_cnt & 1) ^ 1);
+        TR(5);
         tc_fence_after();
         if (has_prev) dq_epilogue(prev_row0);
+        TR(6);
         tmem_st32(t_row + kColP + x * 32, pp);
         tmem_st32(t_row + kColDS + x * 32, pd);
 #pragma unroll
@@ -331,11 +371,14 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.pds_full);
         ++g_cnt;
+        TR(7);
         has_prev = true;
         prev_row0 = (int32_t)((int64_t)it.h * prm.T + it.c0 + i * kTile);
       }
       // dK, dV of this key tile
+      TR(8);
       mbar_wait(&sm.dkv_full, items & 1);
+      TR(9);
       tc_fence_after();
       uint32_t kr[32], vr[32];
       tmem_ld32(t_row + kColDK + x * 32, kr);
@@ -344,21 +387,38 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.dkv_free);
-      if (key_ok) {
+      const float sc = prm.scale;
+      uint32_t pk[16], pv[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        pk[e] = pack_bf16(__uint_as_float(kr[2 * e]) * sc, __uint_as_float(kr[2 * e + 1]) * sc);
+        pv[e] = pack_bf16(__uint_as_float(vr[2 * e]), __uint_as_float(vr[2 * e + 1]));
+      }
+      const int32_t wrow0 = it.tile * kTile + (int32_t)(warp & 3) * 32;   // first key row of this warp
+      if (wrow0 + 32 <= it.L) {
+        // whole warp inside the sequence: stage [32 rows][64 B] x {dK, dV} (64-B swizzle), TMA store
+        stage_free();
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          st_shared_v4(stage_addr + sw64_off(lr, g), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+          st_shared_v4(stage_addr + 2048 + sw64_off(lr, g), pv[4 * g], pv[4 * g + 1], pv[4 * g + 2], pv[4 * g + 3]);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int32_t row = it.c0 + wrow0;
+          tma_store_2d(&tmap_dkv, stage, (H + it.h) * kD + (int32_t)x * 32, row);
+          tma_store_2d(&tmap_dkv, stage + 2048, (2 * H + it.h) * kD + (int32_t)x * 32, row);
+          bulk_commit_group();
+        }
+      } else if (key_ok) {
         const int64_t t = (int64_t)it.c0 + key;
         uint4* dk = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 1) * H + it.h) * kD + x * 32);
         uint4* dv = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 2) * H + it.h) * kD + x * 32);
-        const float sc = prm.scale;
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-          dk[g] = make_uint4(pack_bf16(__uint_as_float(kr[8 * g]) * sc, __uint_as_float(kr[8 * g + 1]) * sc),
-                             pack_bf16(__uint_as_float(kr[8 * g + 2]) * sc, __uint_as_float(kr[8 * g + 3]) * sc),
-                             pack_bf16(__uint_as_float(kr[8 * g + 4]) * sc, __uint_as_float(kr[8 * g + 5]) * sc),
-                             pack_bf16(__uint_as_float(kr[8 * g + 6]) * sc, __uint_as_float(kr[8 * g + 7]) * sc));
-          dv[g] = make_uint4(pack_bf16(__uint_as_float(vr[8 * g]), __uint_as_float(vr[8 * g + 1])),
-                             pack_bf16(__uint_as_float(vr[8 * g + 2]), __uint_as_float(vr[8 * g + 3])),
-                             pack_bf16(__uint_as_float(vr[8 * g + 4]), __uint_as_float(vr[8 * g + 5])),
-                             pack_bf16(__uint_as_float(vr[8 * g + 6]), __uint_as_float(vr[8 * g + 7])));
+          dk[g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+          dv[g] = make_uint4(pv[4 * g], pv[4 * g + 1], pv[4 * g + 2], pv[4 * g + 3]);
         }
       }
     }
@@ -367,7 +427,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       tc_fence_after();
       dq_epilogue(prev_row0);
     }
-    if (threadIdx.x == 128u * x) bulk_wait_group0();
+    if (lane == 0) bulk_wait_group0();
   }
 
   tc_fence_before();
@@ -426,6 +486,12 @@ __global__ void __launch_bounds__(256) bwd_dq_kernel(const float* __restrict__ d
 
 }  // namespace bwd
 
+#ifdef UB_TRACE
+extern "C" __attribute__((visibility("default"))) int ub_debug_bwd_trace(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, bwd::g_trace, bytes < sizeof(bwd::g_trace) ? bytes : sizeof(bwd::g_trace));
+}
+#endif
+
 size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p) {
   return align_up((size_t)p.T * p.heads * 4, 256) + align_up((size_t)p.T * p.heads * 64 * 4, 256);
 }
@@ -433,23 +499,26 @@ size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p) {
 ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* out, const float* lse, const void* dout,
                          const int32_t* d_cu, void* dqkv, void* ws, cudaStream_t s) {
   const bool drop = p.p_dropout > 0.f;
-  auto kern = drop ? bwd::fmha_bwd_kernel<true> : bwd::fmha_bwd_kernel<false>;
+  const bool big = p.B > kPlanCap;
+  auto kern = drop ? (big ? bwd::fmha_bwd_kernel<true, true> : bwd::fmha_bwd_kernel<true, false>)
+                   : (big ? bwd::fmha_bwd_kernel<false, true> : bwd::fmha_bwd_kernel<false, false>);
   UB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmemBytes));
   char* base = static_cast<char*>(ws);
   FmhaPlanView v = fmha_plan_view(base, p.B);
   char* extra = base + align_up(fmha_plan_bytes(p.B), 256);
   float* delta = reinterpret_cast<float*>(extra);
   float* dq_acc = reinterpret_cast<float*>(extra + align_up((size_t)p.T * p.heads * 4, 256));
-  CUtensorMap tq, tdo, tdq, tlse, tdl;
+  CUtensorMap tq, tdo, tdq, tdkv;
   ub_status st = make_tmap_bf16(&tq, qkv, (uint64_t)3 * p.heads * bwd::kD, (uint64_t)p.T,
                                 (uint64_t)3 * p.heads * bwd::kD * 2);
   if (st != UB_OK) return st;
   if ((st = make_tmap_bf16(&tdo, dout, (uint64_t)p.heads * bwd::kD, (uint64_t)p.T, (uint64_t)p.heads * bwd::kD * 2)) !=
       UB_OK)
     return st;
-  if ((st = make_tmap_f32(&tdq, dq_acc, bwd::kD, (uint64_t)p.T * p.heads, bwd::kD * 4, 32, kTile)) != UB_OK) return st;
-  if ((st = make_tmap_f32_1d(&tlse, lse, (uint64_t)p.T * p.heads, kTile)) != UB_OK) return st;
-  if ((st = make_tmap_f32_1d(&tdl, delta, (uint64_t)p.T * p.heads, kTile)) != UB_OK) return st;
+  if ((st = make_tmap_f32(&tdq, dq_acc, bwd::kD, (uint64_t)p.T * p.heads, bwd::kD * 4, 32, 32)) != UB_OK) return st;
+  if ((st = make_tmap_bf16(&tdkv, dqkv, (uint64_t)3 * p.heads * bwd::kD, (uint64_t)p.T,
+                           (uint64_t)3 * p.heads * bwd::kD * 2, 32, 32, 64)) != UB_OK)
+    return st;
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
   if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 1, v, s)) != UB_OK) return st;
   const int64_t rows = p.T * p.heads;
@@ -482,7 +551,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfBwd, 0, s);
-  kern<<<grid, bwd::kThreads, bwd::kSmemBytes, s>>>(tq, tdo, tdq, tlse, tdl, prm);
+  kern<<<grid, bwd::kThreads, bwd::kSmemBytes, s>>>(tq, tdo, tdq, tdkv, prm);
   UB_CHECK_LAUNCH();
   prof_record(kProfBwd, 1, s);
   const int64_t n = rows * (bwd::kD / 8);

@@ -45,9 +45,10 @@ struct PlanSmem {
   int32_t len[kPlanCap];         // length of seq
 };
 
+template <bool kBigB>
 __device__ __forceinline__ void load_plan_smem(PlanSmem& ps, const FmhaPlanView& v, const int32_t* __restrict__ cu,
                                                int32_t B) {
-  if (B > kPlanCap) return;
+  if (kBigB) return;
   for (int k = threadIdx.x; k <= B; k += blockDim.x) {
     ps.prefix[k] = v.item_prefix[k];
     if (k < B) {
@@ -60,10 +61,13 @@ __device__ __forceinline__ void load_plan_smem(PlanSmem& ps, const FmhaPlanView&
   }
 }
 
+// kBigB selects the global-memory decode at compile time: with a runtime branch the compiler
+// hoists the global loads of the fallback above it and every decode pays an L2 round trip.
+template <bool kBigB>
 __device__ __forceinline__ bool decode_item_smem(int32_t w, const PlanSmem& ps, const FmhaPlanView& v,
                                                  const int32_t* __restrict__ cu, int32_t B, int32_t H,
                                                  int32_t tiles_per_item, WorkItem& it) {
-  if (B > kPlanCap) return decode_item(w, v, cu, B, H, tiles_per_item, it);
+  if (kBigB) return decode_item(w, v, cu, B, H, tiles_per_item, it);
   if (w >= ps.prefix[B]) return false;
   int32_t lo = 0, hi = B;
   while (lo < hi) {
@@ -100,7 +104,7 @@ __device__ __forceinline__ uint32_t keep_bits8(uint32_t j0, uint32_t t, uint32_t
 // Host: 2-D bf16 tensor map over a row-major [rows, cols] matrix with row pitch
 // `pitch_bytes`, box {64 cols, 128 rows}, 128-B swizzle (matches sdesc_sw128).
 ub_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
-                         uint32_t box_cols = 64, uint32_t box_rows = 128);
+                         uint32_t box_cols = 64, uint32_t box_rows = 128, int swizzle_bytes = 128);
 // Host: 2-D fp32 tensor map (row-major [rows, cols]), box {box_cols, box_rows}, 128-B swizzle
 // (box_cols * 4 must be 128).
 // Host: 1-D fp32 tensor map over n elements, box of `box` elements (no swizzle).

@@ -32,6 +32,18 @@
 namespace ub {
 namespace fwd {
 
+#ifdef UB_TRACE
+// Debug timeline (trace builds only): CTA 0, lane 0 of every warp records (event, clock64).
+__device__ uint64_t g_trace[10 * 1024];
+#define TR(ev)                                                                                          \
+  do {                                                                                                  \
+    if (blockIdx.x == 0 && lane == 0 && tr_n < 1024)                                                    \
+      g_trace[warp * 1024 + tr_n++] = ((uint64_t)(ev) << 48) | ((uint64_t)clock64() & 0xFFFFFFFFFFFFull); \
+  } while (0)
+#else
+#define TR(ev) do {} while (0)
+#endif
+
 constexpr int kD = 64;
 constexpr int kStages = 3;
 constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
@@ -42,6 +54,7 @@ struct Smem {
   uint8_t q[2][2][kTileBytes];                    // [item slot][warpgroup]
   uint8_t k[kStages][kTileBytes];
   uint8_t v[kStages][kTileBytes];
+  uint8_t ostage[8][32 * 128];                    // per softmax warp: 32 output rows, SW128
   uint64_t q_full[2], q_empty[2];
   uint64_t k_full[kStages], v_full[kStages], kv_empty[kStages];
   uint64_t s_full[2], s_free[2], p_full[2], o_done[2], o_free[2];   // per warpgroup
@@ -71,10 +84,11 @@ __host__ __device__ constexpr uint32_t col_o(int x) { return 256u * x + 192u; }
 // kPoly: number of column pairs out of every 8 whose exp2 runs on the FMA pipe (ex2_poly2).
 // kPack: 0 = bf16 packing by cvt (XU pipe), 1 = integer rounding + byte permute.
 // kDropout: compile the Philox mask in (p > 0) or out (p == 0: no RNG code at all, so the
-// compiler cannot hoist it into the exp loop).
-template <int kPoly, int kPack, bool kDropout>
+// compiler cannot hoist it into the exp loop).  kBigB: batch larger than the smem plan cache.
+template <int kPoly, int kPack, bool kDropout, bool kBigB>
 __global__ void __launch_bounds__(kThreads, 1)
-fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) {
+fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_constant__ CUtensorMap tmap_out,
+                const Params prm) {
   // Taken straight from the __shared__ array so that every access compiles to LDS/STS (a
   // generic pointer would turn them into long-latency generic loads); the dynamic smem
   // window starts 1024-B aligned (checked), as the 128-B swizzle atoms require.
@@ -83,9 +97,12 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
+  uint32_t tr_n = 0;
+  (void)tr_n;
 
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
+    tma_prefetch_desc(&tmap_out);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.q_full[s], 1);
       mbar_init(&sm.q_empty[s], 1);
@@ -102,7 +119,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
     }
     fence_mbar_init();
   }
-  load_plan_smem(sm.plan, prm.plan, prm.cu, prm.B);
+  load_plan_smem<kBigB>(sm.plan, prm.plan, prm.cu, prm.B);
   if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
@@ -117,15 +134,18 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
     if (lane == 0) {
       uint32_t items = 0, kv_it = 0;
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
+      for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
         const uint32_t slot = items & 1;
+        TR(20);
         mbar_wait(&sm.q_empty[slot], ((items >> 1) & 1) ^ 1);
+        TR(21);
         mbar_expect_tx(&sm.q_full[slot], kTileBytes * it.ntile);
         for (int x = 0; x < it.ntile; ++x)
           tma_load_2d(sm.q[slot][x], &tmap_qkv, &sm.q_full[slot], it.h * kD, it.c0 + (it.tile + x) * kTile);
         for (int32_t j = 0; j < it.nt; ++j, ++kv_it) {
           const uint32_t st = kv_it % kStages, ph = (kv_it / kStages) & 1;
           mbar_wait(&sm.kv_empty[st], ph ^ 1);
+          TR(22);
           mbar_expect_tx(&sm.k_full[st], kTileBytes);
           tma_load_2d(sm.k[st], &tmap_qkv, &sm.k_full[st], (H + it.h) * kD, it.c0 + j * kTile);
           mbar_expect_tx(&sm.v_full[st], kTileBytes);
@@ -139,13 +159,16 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
       uint32_t items = 0, kv_it = 0;
       uint32_t s_cnt[2] = {0, 0}, p_cnt[2] = {0, 0}, it_cnt[2] = {0, 0};
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
+      for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
         const uint32_t slot = items & 1;
         const int nx = it.ntile;
+        TR(16);
         mbar_wait(&sm.q_full[slot], (items >> 1) & 1);
+        TR(17);
         tc_fence_after();
         auto issue_s = [&](int x, uint32_t st) {
           mbar_wait(&sm.s_free[x], (s_cnt[x] & 1) ^ 1);
+          TR(10 + x);
           tc_fence_after();
           const uint32_t q_addr = smem_u32(sm.q[slot][x]), k_addr = smem_u32(sm.k[st]);
 #pragma unroll
@@ -158,6 +181,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
         {
           const uint32_t st0 = kv_it % kStages;
           mbar_wait(&sm.k_full[st0], (kv_it / kStages) & 1);
+          TR(18);
           tc_fence_after();
 #pragma unroll
           for (int x = 0; x < 2; ++x)
@@ -167,17 +191,20 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
           const uint32_t cur = kv_it + j, st = cur % kStages, ph = (cur / kStages) & 1;
           const bool has_next = j + 1 < it.nt;
           const uint32_t nst = (cur + 1) % kStages;
+          TR(14);
           if (has_next) {
             mbar_wait(&sm.k_full[nst], ((cur + 1) / kStages) & 1);
             tc_fence_after();
           }
           mbar_wait(&sm.v_full[st], ph);
+          TR(15);
 #pragma unroll
           for (int x = 0; x < 2; ++x) {
             if (x >= nx) break;
             if (has_next) issue_s(x, nst);
             mbar_wait(&sm.p_full[x], p_cnt[x] & 1);
             if (j == 0) mbar_wait(&sm.o_free[x], (it_cnt[x] & 1) ^ 1);
+            TR(12 + x);
             tc_fence_after();
             const uint32_t v_addr = smem_u32(sm.v[st]);
 #pragma unroll
@@ -205,13 +232,15 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
     const uint64_t c2 = f2pack(c, c);
     uint32_t s_cnt = 0, pv_cnt = 0;
     WorkItem it;
-    for (int32_t w = blockIdx.x; decode_item_smem(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x) {
+    for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x) {
       if (x >= it.ntile) continue;
       const int32_t row = (it.tile + x) * kTile + (int32_t)r;
       const uint32_t t_glob = (uint32_t)(it.c0 + row);
       float m_run = -INFINITY, l = 0.f;
       for (int32_t j = 0; j < it.nt; ++j) {
+        TR(1);
         mbar_wait(&sm.s_full[x], s_cnt & 1);
+        TR(2);
         tc_fence_after();
         float s[kTile];
         {
@@ -228,6 +257,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.s_free[x]);
         ++s_cnt;
+        TR(3);
 
         const int32_t kvalid = it.L - j * kTile;
         if (kvalid < kTile) {
@@ -289,6 +319,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
         }
 
         // PV_x(j-1) must have finished reading P and accumulating into O
+        TR(4);
         if (j > 0) {
           mbar_wait(&sm.o_done[x], pv_cnt & 1);
           ++pv_cnt;
@@ -311,6 +342,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
             tmem_st32(t_row + col_o(x) + q * 32, o);
           }
         }
+        TR(5);
         l = fmaf(l, alpha, rs);
         m_run = m_ref;
         tmem_st32(t_row + col_p(x), *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
@@ -319,9 +351,12 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.p_full[x]);
+        TR(6);
       }
       // epilogue: last PV done -> O / l
+      TR(7);
       mbar_wait(&sm.o_done[x], pv_cnt & 1);
+      TR(8);
       ++pv_cnt;
       tc_fence_after();
       uint32_t o0[32], o1[32];
@@ -331,25 +366,42 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.o_free[x]);
-      if (row < it.L) {
+      {
         const float inv = prm.rp / l;
-        uint4* op = reinterpret_cast<uint4*>(prm.out + ((int64_t)t_glob * H + it.h) * kD);
+        uint32_t pk[32];
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          op[g] = make_uint4(pack_bf16(__uint_as_float(o0[8 * g]) * inv, __uint_as_float(o0[8 * g + 1]) * inv),
-                             pack_bf16(__uint_as_float(o0[8 * g + 2]) * inv, __uint_as_float(o0[8 * g + 3]) * inv),
-                             pack_bf16(__uint_as_float(o0[8 * g + 4]) * inv, __uint_as_float(o0[8 * g + 5]) * inv),
-                             pack_bf16(__uint_as_float(o0[8 * g + 6]) * inv, __uint_as_float(o0[8 * g + 7]) * inv));
-          op[4 + g] = make_uint4(pack_bf16(__uint_as_float(o1[8 * g]) * inv, __uint_as_float(o1[8 * g + 1]) * inv),
-                                 pack_bf16(__uint_as_float(o1[8 * g + 2]) * inv, __uint_as_float(o1[8 * g + 3]) * inv),
-                                 pack_bf16(__uint_as_float(o1[8 * g + 4]) * inv, __uint_as_float(o1[8 * g + 5]) * inv),
-                                 pack_bf16(__uint_as_float(o1[8 * g + 6]) * inv, __uint_as_float(o1[8 * g + 7]) * inv));
+        for (int e = 0; e < 16; ++e) {
+          pk[e] = pack_bf16(__uint_as_float(o0[2 * e]) * inv, __uint_as_float(o0[2 * e + 1]) * inv);
+          pk[16 + e] = pack_bf16(__uint_as_float(o1[2 * e]) * inv, __uint_as_float(o1[2 * e + 1]) * inv);
         }
-        prm.lse[(int64_t)it.h * prm.T + t_glob] = m_run * prm.scale + logf(l);
+        const int32_t wrow0 = (it.tile + x) * kTile + (int32_t)(warp & 3) * 32;   // first row of this warp
+        if (wrow0 + 32 <= it.L) {
+          // whole warp inside the sequence: stage 32 rows (128-B swizzle) and TMA-store them
+          uint8_t* stage = sm.ostage[warp];
+          const uint32_t sa = smem_u32(stage);
+          if (lane == 0) bulk_wait_group_read0();          // previous store of this warp has read it
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            st_shared_v4(sa + sw128_off(lane, g), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_out, stage, it.h * kD, it.c0 + wrow0);
+            bulk_commit_group();
+          }
+        } else if (row < it.L) {
+          uint4* op = reinterpret_cast<uint4*>(prm.out + ((int64_t)t_glob * H + it.h) * kD);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) op[g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+        }
+        if (row < it.L) prm.lse[(int64_t)it.h * prm.T + t_glob] = m_run * prm.scale + logf(l);
       }
+      TR(9);
     }
   }
 
+  if (warp < 8 && lane == 0) bulk_wait_group0();        // output stores complete before exit
   tc_fence_before();
   __syncthreads();
   if (warp == 9) {
@@ -360,41 +412,39 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const Params prm) 
 
 }  // namespace fwd
 
+#ifdef UB_TRACE
+extern "C" __attribute__((visibility("default"))) int ub_debug_fwd_trace(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, fwd::g_trace, bytes < sizeof(fwd::g_trace) ? bytes : sizeof(fwd::g_trace));
+}
+#endif
+
 static int env_int(const char* name, int dflt, int lo, int hi) {
   const char* e = std::getenv(name);
   int v = e ? std::atoi(e) : dflt;
   return (v < lo || v > hi) ? dflt : v;
 }
 
-template <int P, int K>
-static void (*pick_fwd(bool drop))(CUtensorMap, fwd::Params) {
-  return drop ? fwd::fmha_fwd_kernel<P, K, true> : fwd::fmha_fwd_kernel<P, K, false>;
+template <int P>
+static void (*pick_fwd(bool drop, bool big))(CUtensorMap, CUtensorMap, fwd::Params) {
+  if (big) return drop ? fwd::fmha_fwd_kernel<P, 0, true, true> : fwd::fmha_fwd_kernel<P, 0, false, true>;
+  return drop ? fwd::fmha_fwd_kernel<P, 0, true, false> : fwd::fmha_fwd_kernel<P, 0, false, false>;
 }
 
 ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out, float* lse,
                          void* ws, cudaStream_t s) {
-  // tuning knobs (measured defaults; env overrides are for sweeps)
-  static const int poly = env_int("UB_FWD_POLY", 2, 0, 4);
-  static const int pack = env_int("UB_FWD_PACK", 0, 0, 1);
-  const bool drop = p.p_dropout > 0.f;
-  void (*kern)(CUtensorMap, fwd::Params);
-  switch (poly * 2 + pack) {
-    case 0: kern = pick_fwd<0, 0>(drop); break;
-    case 1: kern = pick_fwd<0, 1>(drop); break;
-    case 2: kern = pick_fwd<1, 0>(drop); break;
-    case 3: kern = pick_fwd<1, 1>(drop); break;
-    case 4: kern = pick_fwd<2, 0>(drop); break;
-    case 5: kern = pick_fwd<2, 1>(drop); break;
-    case 6: kern = pick_fwd<3, 0>(drop); break;
-    case 7: kern = pick_fwd<3, 1>(drop); break;
-    case 8: kern = pick_fwd<4, 0>(drop); break;
-    default: kern = pick_fwd<4, 1>(drop); break;
-  }
+  // tuning knob: fraction (x/8) of exp2 pairs on the FMA pipe, 0 or 2 (measured default 2)
+  static const int poly = env_int("UB_FWD_POLY", 2, 0, 4) >= 2 ? 2 : 0;
+  const bool drop = p.p_dropout > 0.f, big = p.B > kPlanCap;
+  void (*kern)(CUtensorMap, CUtensorMap, fwd::Params) = poly == 2 ? pick_fwd<2>(drop, big) : pick_fwd<0>(drop, big);
   UB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::kSmemBytes));
   CUtensorMap tmap;
   ub_status st = make_tmap_bf16(&tmap, qkv, (uint64_t)3 * p.heads * fwd::kD, (uint64_t)p.T,
                                 (uint64_t)3 * p.heads * fwd::kD * 2);
   if (st != UB_OK) return st;
+  CUtensorMap tmap_out;
+  if ((st = make_tmap_bf16(&tmap_out, out, (uint64_t)p.heads * fwd::kD, (uint64_t)p.T, (uint64_t)p.heads * fwd::kD * 2,
+                           64, 32, 128)) != UB_OK)
+    return st;
   FmhaPlanView v = fmha_plan_view(ws, p.B);
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
   if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 2, v, s)) != UB_OK) return st;
@@ -422,7 +472,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfFwd, 0, s);
-  kern<<<grid, fwd::kThreads, fwd::kSmemBytes, s>>>(tmap, prm);
+  kern<<<grid, fwd::kThreads, fwd::kSmemBytes, s>>>(tmap, tmap_out, prm);
   UB_CHECK_LAUNCH();
   prof_record(kProfFwd, 1, s);
   return UB_OK;
