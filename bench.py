@@ -41,7 +41,7 @@ H, D, S, B = 16, 64, 512, 56
 REC = 16      # per-token record: input_id, segment_id, masked_lm_label, position (int32 x 4)
 SREC = 4      # per-sample record: next_sentence_label (int32)
 N_SETS = 3    # rotating input sets: each step's working set (> 300 MB) and the 2 others exceed L2
-KERNELS_PER_STEP = 10   # ours: unpad, 2x exchange copy, fwd plan+main, bwd plan+pre+main+dq, pad
+KERNELS_PER_STEP = 9    # ours: unpad, 2x exchange copy, fwd plan+main, bwd plan+pre+main, pad
 
 
 def parse():
@@ -407,6 +407,7 @@ def run_ours(args, world, rank, local):
     fmha_only = mean_T * world / ((fwd_us + bwd_us) * 1e-6)
 
     e2e = None if args.no_e2e else run_e2e(args, wl, world)
+    gather = gather_bench(wl, peaks) if rank == 0 else None
     out = {"metric": "unpadded FMHA fwd+bwd tokens/s (BERT-large)", "value": round(value, 1), "unit": "tokens/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -416,10 +417,62 @@ def run_ours(args, world, rank, local):
                       "parallelism": f"dp{world}", "fmha_ctas": wl.ctas, "l2": "rotating 3 input sets; per-step working set > L2",
                       "step": "unpad records + exchange (side stream) | fmha fwd + bwd + pad (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
-           "imbalance": round(imbalance, 5), "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk}
+           "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
+           "gather": gather, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk}
     if e2e is not None:
         out["e2e"] = e2e
     return out, wl
+
+
+def gather_bench(wl, peaks, iters=20):
+    """a6 / a9 on the config-2 hidden state (bf16 [56, 512, 1024] <-> [T, 1024]), HBM-bound:
+    algorithmic bytes unpad = 2*T*row, pad = T*row + B*S*row; 3 rotating buffer sets."""
+    ub = wl.ub
+    st = wl.sets[0]
+    T, cu = st["T"], st["cu_local"]
+    row = H * D * 2
+    bufs = [(torch.randn((B, S, H * D), device=wl.dev).to(torch.bfloat16),
+             torch.empty((T, H * D), dtype=torch.bfloat16, device=wl.dev)) for _ in range(3)]
+    out = {}
+    for name, fn, nbytes in (("unpad", lambda b: ub.unpad(b[0], cu, T, out=b[1]), 2 * T * row),
+                             ("pad", lambda b: ub.pad(b[1], cu, B, S, out=b[0]), T * row + B * S * row)):
+        for k in range(3):
+            fn(bufs[k])
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        for k in range(iters):
+            ev[k][0].record()
+            fn(bufs[k % 3])
+            ev[k][1].record()
+        torch.cuda.synchronize()
+        us = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
+        gbs = nbytes / (us * 1e-6) / 1e9
+        out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
+                     "bytes": int(nbytes)}
+    out["shape"] = f"hidden [{B}, {S}, {H * D}] bf16 <-> [T={T}, {H * D}]"
+    return out
+
+
+def planned_imbalance(args, steps=20):
+    """Token imbalance (max/mean - 1) that the library's planner (ub_balance_plan, the code
+    the exchange runs) produces for W = 2, 4, 8 ranks of 56 sequences; 'before' = no
+    exchange.  A pure function of the plan, so it is exact without 8 GPUs."""
+    from paper_2208_08124_b200 import api
+    out = {}
+    for W in (2, 4, 8):
+        rec = {"before": [], "paper": [], "snake": []}
+        for skew in ("iid", "sorted-block"):
+            for k in range(steps):
+                a = synth.skewed_rank_lengths(W, B, 1000 + k, skew, args.dist)
+                tok = a.sum(axis=1).astype(np.float64)
+                rec["before"].append(tok.max() / tok.mean() - 1)
+                for mode in ("paper", "snake"):
+                    rt = api.balance_plan(a.reshape(-1), W, B, S, mode)["rank_tokens"].astype(np.float64)
+                    rec[mode].append(rt.max() / rt.mean() - 1)
+        out[f"w{W}"] = {k: {"mean": round(float(np.mean(v)), 5), "max": round(float(np.max(v)), 5)}
+                        for k, v in rec.items()}
+    out["note"] = f"{steps} steps x (iid, sorted-block) skews, {args.dist}, B={B}/rank"
+    return out
 
 
 def _patch_lse(wl, n):

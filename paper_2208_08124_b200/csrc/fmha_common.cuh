@@ -11,6 +11,7 @@ namespace ub {
 
 struct WorkItem {
   int32_t b, h, tile, c0, L, nt, ntile;   // tile = first tile of the item, ntile = tiles in it
+  int32_t pc0;                            // tile-padded row base of the sequence
 };
 
 // Map a flat work index onto (sequence, head, tile group) along the bucketed plan.
@@ -28,6 +29,13 @@ __device__ __forceinline__ bool decode_item(int32_t w, const FmhaPlanView& v, co
   it.c0 = cu[it.b];
   it.L = cu[it.b + 1] - it.c0;
   it.nt = (it.L + kTile - 1) / kTile;
+  it.pc0 = v.pad_c0[it.b];
+  if (tiles_per_item == 0) {
+    it.h = local;
+    it.tile = 0;
+    it.ntile = it.nt;
+    return true;
+  }
   const int32_t ngroups = (it.nt + tiles_per_item - 1) / tiles_per_item;
   it.h = local / ngroups;
   it.tile = (local - it.h * ngroups) * tiles_per_item;
@@ -43,6 +51,7 @@ struct PlanSmem {
   int32_t seq[kPlanCap];         // sequence id
   int32_t c0[kPlanCap];          // cu_seqlens[seq]
   int32_t len[kPlanCap];         // length of seq
+  int32_t pc0[kPlanCap];         // tile-padded row base of seq
 };
 
 template <bool kBigB>
@@ -57,6 +66,7 @@ __device__ __forceinline__ void load_plan_smem(PlanSmem& ps, const FmhaPlanView&
       ps.seq[k] = b;
       ps.c0[k] = a;
       ps.len[k] = cu[b + 1] - a;
+      ps.pc0[k] = v.pad_c0[b];
     }
   }
 }
@@ -78,7 +88,14 @@ __device__ __forceinline__ bool decode_item_smem(int32_t w, const PlanSmem& ps, 
   const int32_t local = w - ps.prefix[lo];
   it.c0 = ps.c0[lo];
   it.L = ps.len[lo];
+  it.pc0 = ps.pc0[lo];
   it.nt = (it.L + kTile - 1) / kTile;
+  if (tiles_per_item == 0) {
+    it.h = local;
+    it.tile = 0;
+    it.ntile = it.nt;
+    return true;
+  }
   const int32_t ngroups = (it.nt + tiles_per_item - 1) / tiles_per_item;
   it.h = local / ngroups;
   it.tile = (local - it.h * ngroups) * tiles_per_item;

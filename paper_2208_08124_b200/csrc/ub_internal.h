@@ -47,7 +47,8 @@ constexpr int kTile = 128;  // query / key tile (rows) of the tensor-core path a
 
 struct FmhaPlanView {   // device views into the workspace, filled by the plan kernel
   int32_t* seq_order;   // [B] sequences sorted by tile count desc (then id asc)
-  int32_t* item_prefix; // [B+1] prefix of items (tiles * H) along seq_order
+  int32_t* item_prefix; // [B+1] prefix of items along seq_order
+  int32_t* pad_c0;      // [B+1] per sequence (original order): sum of 128 * tiles of the earlier ones
   int32_t* counters;    // [4] scheduler counters
 };
 
