@@ -3,6 +3,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "ub_internal.h"
 
@@ -36,6 +38,19 @@ ub_status require_sm100() {
   }
   if (cached[dev] != 100)
     return set_error(UB_ERR_UNSUPPORTED, "this library is built for sm_100a (B200); device is sm_%d", cached[dev]);
+  return UB_OK;
+}
+
+ub_status smem_attr_once(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  UB_CHECK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : done)
+    if (e.first == func && e.second == dev) return UB_OK;
+  UB_CHECK_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.emplace_back(func, dev);
   return UB_OK;
 }
 

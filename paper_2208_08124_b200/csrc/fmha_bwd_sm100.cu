@@ -74,7 +74,7 @@ struct Params {
   const float* lse;     // [H, T]
   const float* delta;   // [H, T]
   __nv_bfloat16* dqkv;  // [T, 3, H, 64]
-  int32_t B, H;
+  int32_t B, H, max_tiles;
   int64_t T;
   float scale, scale_log2;
   float rp;
@@ -135,7 +135,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     mbar_init(&sm.dkv_free, 8);
     fence_mbar_init();
   }
-  load_plan_smem<kBigB>(sm.plan, prm.plan, prm.cu, prm.B);
+  if (!kBigB && warp == 8) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 1, lane);
   if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
@@ -502,7 +502,10 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   const bool big = p.B > kPlanCap;
   auto kern = drop ? (big ? bwd::fmha_bwd_kernel<true, true> : bwd::fmha_bwd_kernel<true, false>)
                    : (big ? bwd::fmha_bwd_kernel<false, true> : bwd::fmha_bwd_kernel<false, false>);
-  UB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd::kSmemBytes));
+  {
+    const ub_status sa = smem_attr_once(reinterpret_cast<const void*>(kern), (int)bwd::kSmemBytes);
+    if (sa != UB_OK) return sa;
+  }
   char* base = static_cast<char*>(ws);
   FmhaPlanView v = fmha_plan_view(base, p.B);
   char* extra = base + align_up(fmha_plan_bytes(p.B), 256);
@@ -520,7 +523,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
                            (uint64_t)3 * p.heads * bwd::kD * 2, 32, 32, 64)) != UB_OK)
     return st;
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
-  if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 1, v, s)) != UB_OK) return st;
+  if (p.B > kPlanCap && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 1, v, s)) != UB_OK) return st;
   const int64_t rows = p.T * p.heads;
   const int64_t n_acc4 = rows * bwd::kD / 4;
   bwd::bwd_pre_kernel<<<(unsigned)((rows * 8 + 255) / 256), 256, 0, s>>>(
@@ -536,6 +539,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   prm.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   prm.B = p.B;
   prm.H = p.heads;
+  prm.max_tiles = max_tiles;
   prm.T = p.T;
   prm.scale = p.scale;
   prm.scale_log2 = p.scale * 1.4426950408889634f;

@@ -43,32 +43,64 @@ __device__ __forceinline__ bool decode_item(int32_t w, const FmhaPlanView& v, co
   return true;
 }
 
-// Shared-memory copy of the plan (one per CTA, loaded once at kernel start) so that work
-// decoding costs a few shared loads instead of a chain of dependent L2 loads per item.
-constexpr int kPlanCap = 1024;   // sequences; larger batches decode from global memory
+// The plan built by each CTA in shared memory (B <= kPlanCap): one warp buckets the
+// sequences by 128-token tile count exactly like fmha_plan_kernel and writes the item
+// prefix, so the persistent kernels need no separate planning launch and decode a work
+// item with a few shared loads.  Larger batches use fmha_plan_kernel + global decode.
+constexpr int kPlanCap = 1024;
 struct PlanSmem {
   int32_t prefix[kPlanCap + 1];  // item prefix along the bucketed order
   int32_t seq[kPlanCap];         // sequence id
   int32_t c0[kPlanCap];          // cu_seqlens[seq]
   int32_t len[kPlanCap];         // length of seq
-  int32_t pc0[kPlanCap];         // tile-padded row base of seq
 };
 
-template <bool kBigB>
-__device__ __forceinline__ void load_plan_smem(PlanSmem& ps, const FmhaPlanView& v, const int32_t* __restrict__ cu,
-                                               int32_t B) {
-  if (kBigB) return;
-  for (int k = threadIdx.x; k <= B; k += blockDim.x) {
-    ps.prefix[k] = v.item_prefix[k];
-    if (k < B) {
-      const int32_t b = v.seq_order[k];
-      const int32_t a = cu[b];
-      ps.seq[k] = b;
-      ps.c0[k] = a;
-      ps.len[k] = cu[b + 1] - a;
-      ps.pc0[k] = v.pad_c0[b];
+// executed by all 32 lanes of one warp
+__device__ __forceinline__ void build_plan_smem(PlanSmem& ps, const int32_t* __restrict__ cu, int32_t B, int32_t H,
+                                                int32_t max_tiles, int32_t tiles_per_item, uint32_t lane) {
+  const uint32_t lt = (1u << lane) - 1u;
+  int32_t base = 0;
+  for (int32_t c = max_tiles; c >= 0; --c) {
+    for (int32_t b0 = 0; b0 < B; b0 += 32) {
+      const int32_t b = b0 + (int32_t)lane;
+      int32_t bucket = -1, a = 0, L = 0;
+      if (b < B) {
+        a = cu[b];
+        L = cu[b + 1] - a;
+        const int32_t nt = (L + kTile - 1) / kTile;
+        bucket = nt < max_tiles ? (nt < 0 ? 0 : nt) : max_tiles;
+      }
+      const bool flag = bucket == c;
+      const uint32_t bal = __ballot_sync(0xffffffffu, flag);
+      if (flag) {
+        const int32_t pos = base + __popc(bal & lt);
+        ps.seq[pos] = b;
+        ps.c0[pos] = a;
+        ps.len[pos] = L;
+      }
+      base += __popc(bal);
     }
   }
+  __syncwarp();
+  int32_t running = 0;
+  for (int32_t k0 = 0; k0 < B; k0 += 32) {
+    const int32_t k = k0 + (int32_t)lane;
+    int32_t items = 0;
+    if (k < B) {
+      const int32_t L = ps.len[k];
+      const int32_t nt = L > 0 ? (L + kTile - 1) / kTile : 0;
+      items = (tiles_per_item > 0 ? (nt + tiles_per_item - 1) / tiles_per_item : (nt > 0 ? 1 : 0)) * H;
+    }
+    int32_t incl = items;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += y;
+    }
+    if (k < B) ps.prefix[k] = running + incl - items;
+    running += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) ps.prefix[B] = running;
 }
 
 // kBigB selects the global-memory decode at compile time: with a runtime branch the compiler
@@ -88,7 +120,7 @@ __device__ __forceinline__ bool decode_item_smem(int32_t w, const PlanSmem& ps, 
   const int32_t local = w - ps.prefix[lo];
   it.c0 = ps.c0[lo];
   it.L = ps.len[lo];
-  it.pc0 = ps.pc0[lo];
+  it.pc0 = 0;
   it.nt = (it.L + kTile - 1) / kTile;
   if (tiles_per_item == 0) {
     it.h = local;

@@ -68,7 +68,7 @@ struct Params {
   FmhaPlanView plan;
   __nv_bfloat16* out;
   float* lse;
-  int32_t B, H;
+  int32_t B, H, max_tiles;
   int64_t T;
   float scale, scale_log2;
   float rp;           // 1 / (1 - p)
@@ -119,7 +119,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     }
     fence_mbar_init();
   }
-  load_plan_smem<kBigB>(sm.plan, prm.plan, prm.cu, prm.B);
+  if (!kBigB && warp == 8) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 2, lane);
   if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
@@ -436,7 +436,10 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   static const int poly = env_int("UB_FWD_POLY", 2, 0, 4) >= 2 ? 2 : 0;
   const bool drop = p.p_dropout > 0.f, big = p.B > kPlanCap;
   void (*kern)(CUtensorMap, CUtensorMap, fwd::Params) = poly == 2 ? pick_fwd<2>(drop, big) : pick_fwd<0>(drop, big);
-  UB_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd::kSmemBytes));
+  {
+    const ub_status sa = smem_attr_once(reinterpret_cast<const void*>(kern), (int)fwd::kSmemBytes);
+    if (sa != UB_OK) return sa;
+  }
   CUtensorMap tmap;
   ub_status st = make_tmap_bf16(&tmap, qkv, (uint64_t)3 * p.heads * fwd::kD, (uint64_t)p.T,
                                 (uint64_t)3 * p.heads * fwd::kD * 2);
@@ -447,7 +450,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
     return st;
   FmhaPlanView v = fmha_plan_view(ws, p.B);
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
-  if ((st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 2, v, s)) != UB_OK) return st;
+  if (p.B > kPlanCap && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 2, v, s)) != UB_OK) return st;
 
   fwd::Params prm{};
   prm.cu = d_cu;
@@ -456,6 +459,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   prm.lse = lse;
   prm.B = p.B;
   prm.H = p.heads;
+  prm.max_tiles = max_tiles;
   prm.T = p.T;
   prm.scale = p.scale;
   prm.scale_log2 = p.scale * 1.4426950408889634f;

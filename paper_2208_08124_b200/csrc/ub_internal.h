@@ -19,6 +19,9 @@ ub_status require_sm100();
 enum ProfKernel { kProfFwd = 0, kProfBwd = 1, kProfPad = 2, kProfUnpad = 3, kProfCount = 4 };
 void prof_record(int kernel_id, int which, cudaStream_t s);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device).
+ub_status smem_attr_once(const void* func, int bytes);
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 #define UB_CHECK_CUDA(expr)                                                              \
