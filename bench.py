@@ -3,10 +3,12 @@
 
 A step is one pass of every row of SURVEY.md §8(a) over one 56-sequence BERT-large batch
 per GPU (H=16, D=64, max_seqlen 512, MLPerf-like length mix, bf16):
-  side stream (prepared one step ahead):
+  side stream (while step n computes, step n+1 is exchanged and the lengths of
+  step n+2 are gathered, so the host never waits on work it has just enqueued):
+    a1         exchange_begin: NCCL all-gather of lengths + D2H into a pinned slot
     a6 unpad   padded input records [56, 512, 16 B] -> packed [T, 16 B]
-    a1-a5      balance_exchange: NCCL all-gather of lengths, host plan (sort + interleave,
-               P:355-359), pack, grouped ncclSend/ncclRecv, reorder, cu_seqlens H2D
+    a2-a5      exchange_finish: host plan (sort + interleave), pack, grouped
+               ncclSend/ncclRecv, reorder, cu_seqlens H2D
   main stream:
     a7 varlen FMHA forward over the exchanged cu_seqlens
     a8 varlen FMHA backward (dO given)
@@ -41,6 +43,8 @@ H, D, S, B = 16, 64, 512, 56
 REC = 16      # per-token record: input_id, segment_id, masked_lm_label, position (int32 x 4)
 SREC = 4      # per-sample record: next_sentence_label (int32)
 N_SETS = 3    # rotating input sets: each step's working set (> 300 MB) and the 2 others exceed L2
+N_EX = 4      # exchange output buffers in flight: the side stream never waits on the step just enqueued
+PIPE = 2      # step n computes while step n+PIPE is exchanged and n+PIPE+1's lengths are gathered
 KERNELS_PER_STEP = 8    # ours: unpad, 2x exchange copy, fwd main, bwd pre+main+dq-finalize, pad
 
 
@@ -283,35 +287,44 @@ class Workload:
         self.packed_recs = torch.empty((self.cap, 4), dtype=torch.int32, device=dev)
         self.ex = [{"tokens": torch.empty((self.cap, 4), dtype=torch.int32, device=dev),
                     "samples": torch.empty((B, 1), dtype=torch.int32, device=dev),
-                    "cu": torch.empty(B + 1, dtype=torch.int32, device=dev), "T": 0, "L": None} for _ in range(2)]
+                    "cu": torch.empty(B + 1, dtype=torch.int32, device=dev), "T": 0, "L": None} for _ in range(N_EX)]
         self.out = torch.empty((self.cap, H, D), dtype=torch.bfloat16, device=dev)
         self.lse = torch.empty((H, self.cap), dtype=torch.float32, device=dev)
         self.dqkv = torch.empty((self.cap, 3, H, D), dtype=torch.bfloat16, device=dev)
         self.padded_out = torch.empty((B, S, H, D), dtype=torch.bfloat16, device=dev)
         self.main = torch.cuda.current_stream()
         self.side = torch.cuda.Stream()
-        self.ex_ready = [torch.cuda.Event() for _ in range(2)]
-        self.done = [torch.cuda.Event() for _ in range(2)]
+        self.ex_ready = [torch.cuda.Event() for _ in range(N_EX)]
+        self.done = [torch.cuda.Event() for _ in range(N_EX)]
         self.comm = ub.Comm(world, rank)
         # leave SMs free for the side-stream exchange (NCCL + copy kernels) to run
         # concurrently with the persistent FMHA kernels (P:376-381 overlap)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.ctas = sms - args.reserve_sms
 
-    def prepare(self, n):
-        """Side stream, one step ahead: a6 unpad of step n's input records, a1-a5 exchange."""
-        st, ex = self.sets[n % N_SETS], self.ex[n % 2]
-        self.side.wait_event(self.done[n % 2])            # step n-2 finished with these buffers
-        with torch.cuda.stream(self.side):
-            self.ub.unpad(st["padded_recs"], st["cu_local"], st["T"], out=self.packed_recs[:st["T"]],
-                          stream=self.side)
-            _, _, _, T, perm = self.comm.balance_exchange(
-                st["lengths"], self.packed_recs[:st["T"]], st["samples"], self.cap, S, self.args.balance,
-                out_tokens=ex["tokens"], out_samples=ex["samples"], out_cu=ex["cu"], stream=self.side)
+    def begin(self, n):
+        """Side stream, two steps ahead: a1 all-gather of step n's lengths (no host wait)."""
+        st = self.sets[n % N_SETS]
+        self.comm.exchange_begin(n % self.comm.SLOTS, st["lengths"], self.cap, REC, SREC, stream=self.side)
+
+    def finish(self, n, marks=None):
+        """Side stream, one step ahead: a6 unpad of step n's input records, a2-a5 plan and
+        exchange.  Its one host wait is for the lengths begin(n) fetched a step earlier."""
+        st, ex = self.sets[n % N_SETS], self.ex[n % N_EX]
+        self.side.wait_event(self.done[n % N_EX])         # step n-N_EX finished with these buffers
+        self.ub.unpad(st["padded_recs"], st["cu_local"], st["T"], out=self.packed_recs[:st["T"]],
+                      stream=self.side)
+        if marks is not None:
+            marks.append(time.perf_counter())
+        T, perm = self.comm.exchange_finish(n % self.comm.SLOTS, B, self.packed_recs[:st["T"]], st["samples"],
+                                            self.cap, S, self.args.balance, ex["tokens"], ex["samples"], ex["cu"],
+                                            stream=self.side)
         allL = np.asarray(self.all_lengths_cache(n), np.int64)
         ex["T"] = T
         ex["L"] = allL[perm[self.rank * B:(self.rank + 1) * B]]
-        self.ex_ready[n % 2].record(self.side)
+        self.ex_ready[n % N_EX].record(self.side)
+        if marks is not None:
+            marks.append(time.perf_counter())
 
     def all_lengths_cache(self, n):
         s = n % N_SETS
@@ -321,21 +334,39 @@ class Workload:
             self._all_l[s] = synth.skewed_rank_lengths(self.world, B, s, self.args.skew, self.args.dist).reshape(-1)
         return self._all_l[s]
 
-    def step(self, n, prof=None):
-        """Main stream: a7 fwd, a8 bwd, a9 pad for step n."""
-        st, ex = self.sets[n % N_SETS], self.ex[n % 2]
+    def view(self, owner, key, T):
+        """owner[key][:T], cached (slicing a tensor costs ~1.5 us of host time)."""
+        d = owner.setdefault("_views", {}) if isinstance(owner, dict) else self.__dict__.setdefault("_views", {})
+        k = (key, T, id(owner[key] if isinstance(owner, dict) else getattr(owner, key)))
+        v = d.get(k)
+        if v is None:
+            v = d[k] = (owner[key] if isinstance(owner, dict) else getattr(owner, key))[:T]
+        return v
+
+    def step(self, n, prof=None, marks=None):
+        """Main stream: a7 fwd, a8 bwd, a9 pad for step n.  marks: host timestamps."""
+        st, ex = self.sets[n % N_SETS], self.ex[n % N_EX]
         T = ex["T"]
-        self.main.wait_event(self.ex_ready[n % 2])
+        self.main.wait_event(self.ex_ready[n % N_EX])
         p = self.args.p_dropout
         if prof is not None:
             for kid, pair in prof.items():
                 self.ub.api.profile_events(kid, *pair)
-        self.ub.varlen_fmha_fwd(st["qkv"][:T], ex["cu"], S, None, p, 0x2208 + n, 0, out=self.out[:T],
-                                lse=self.lse, num_ctas=self.ctas)
-        self.ub.varlen_fmha_bwd(st["qkv"][:T], self.out[:T], self.lse, st["dout"][:T], ex["cu"], S, None, p,
-                                0x2208 + n, 0, dqkv=self.dqkv[:T], num_ctas=self.ctas)
-        self.ub.pad(self.out[:T], ex["cu"], B, S, out=self.padded_out)
-        self.done[n % 2].record(self.main)
+        if marks is not None:
+            marks.append(time.perf_counter())
+        qkv, out = self.view(st, "qkv", T), self.view(self, "out", T)
+        self.ub.varlen_fmha_fwd(qkv, ex["cu"], S, None, p, 0x2208 + n, 0, out=out, lse=self.lse, num_ctas=self.ctas,
+                                stream=self.main)
+        if marks is not None:
+            marks.append(time.perf_counter())
+        self.ub.varlen_fmha_bwd(qkv, out, self.lse, self.view(st, "dout", T), ex["cu"], S, None, p, 0x2208 + n, 0,
+                                dqkv=self.view(self, "dqkv", T), num_ctas=self.ctas, stream=self.main)
+        if marks is not None:
+            marks.append(time.perf_counter())
+        self.ub.pad(out, ex["cu"], B, S, out=self.padded_out, stream=self.main)
+        self.done[n % N_EX].record(self.main)
+        if marks is not None:
+            marks.append(time.perf_counter())
         return T
 
 
@@ -344,18 +375,27 @@ def run_ours(args, world, rank, local):
     wl = Workload(args, world, rank, dev)
     ub = wl.ub
     peaks = load_peaks()
-    # warm-up
-    wl.prepare(0)
+    # warm-up.  Pipeline: step n computes (main) while n+PIPE is exchanged and the lengths of
+    # n+PIPE+1 are gathered (side stream)
+    for n in range(PIPE + 1):
+        wl.begin(n)
+    for n in range(PIPE):
+        wl.finish(n)
     for n in range(args.warmup):
         _patch_lse(wl, n)
         wl.step(n)
-        wl.prepare(n + 1)
+        wl.finish(n + PIPE)
+        wl.begin(n + PIPE + 1)
     torch.cuda.synchronize()
     barrier(world)
     # timed region
     kids = [ub.api.PROF_FWD, ub.api.PROF_BWD, ub.api.PROF_PAD, ub.api.PROF_UNPAD]
     prof_events = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in kids}
                    for _ in range(args.steps)]
+    for d in prof_events:                 # create the cudaEvent_t handles outside the timed loop
+        for a, b_ in d.values():
+            a.record(wl.main)
+            b_.record(wl.main)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -363,25 +403,31 @@ def run_ours(args, world, rank, local):
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tokens, lens_used = 0, []
-    host_step, host_prep = [], []
+    host_step, host_prep, marks = [], [], []
     e0.record(wl.main)
     for k in range(args.steps):
         n = args.warmup + k
         h0 = time.perf_counter()
         _patch_lse(wl, n)
-        tokens += wl.step(n, prof_events[k])
-        lens_used.append(wl.ex[n % 2]["L"])
+        m = []
+        tokens += wl.step(n, prof_events[k], m)
+        lens_used.append(wl.ex[n % N_EX]["L"])
         h1 = time.perf_counter()
-        wl.prepare(n + 1)
+        wl.finish(n + PIPE, m)
+        wl.begin(n + PIPE + 1)
+        m.append(time.perf_counter())
+        marks.append(np.diff([h0] + m))
         host_step.append(h1 - h0)
         host_prep.append(time.perf_counter() - h1)
-    wl.main.wait_event(wl.ex_ready[(args.warmup + args.steps) % 2])
+    wl.main.wait_stream(wl.side)      # steady state: the K steps plus the exchange of the next one
     e1.record(wl.main)
     torch.cuda.synchronize()
     barrier(world)
     clk = clocks.stop()
     for kid in kids:
         ub.api.profile_events(kid)
+    wl.finish(args.warmup + args.steps + PIPE)  # drain the begin still in flight (untimed)
+    torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     ms_max = all_max(ms, world)
     tok_all = all_sum(tokens, world)
@@ -428,8 +474,11 @@ def run_ours(args, world, rank, local):
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
            "gather": gather, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
-           "host_us_per_step": {"enqueue_compute": round(1e6 * float(np.mean(host_step)), 1),
-                                "exchange_call": round(1e6 * float(np.mean(host_prep)), 1)}}
+           "host_us_per_step": dict(zip(["step_setup", "fwd_call", "bwd_call", "pad_call", "unpad_call", "finish_call",
+                                              "begin_call"],
+                                        [round(1e6 * float(x), 1) for x in np.median(np.array(marks), axis=0)]),
+                                    enqueue_compute=round(1e6 * float(np.median(host_step)), 1),
+                                    exchange_calls=round(1e6 * float(np.median(host_prep)), 1))}
     if e2e is not None:
         out["e2e"] = e2e
     return out, wl
@@ -488,7 +537,7 @@ def planned_imbalance(args, steps=20):
 
 def _patch_lse(wl, n):
     """The ABI wants lse as a dense [H, T] array: view the front of the buffer per step."""
-    T = wl.ex[n % 2]["T"]
+    T = wl.ex[n % N_EX]["T"]
     if not hasattr(wl, "lse_full"):
         wl.lse_full = wl.lse
     wl.lse = wl.lse_full.view(-1)[:H * max(T, 1)].view(H, max(T, 1))
@@ -497,50 +546,97 @@ def _patch_lse(wl, n):
 def run_e2e(args, wl, world):
     """Same step through the public API with HOST inputs: per step the padded input
     records, lengths, sample records, qkv and dO are copied H2D from pinned memory and the
-    step's result (dqkv) is read back D2H, all inside the timed region."""
+    step's result (dqkv) is read back D2H, all inside the timed region.  Copies run on their
+    own streams (H2D of step n+1 and D2H of step n-1 overlap step n's kernels), so the
+    number is bound by PCIe, as a data-loading pipeline would be."""
     host = []
     for s in range(N_SETS):
         st = wl.sets[s]
-        T = st["T"]
         host.append({"recs": st["padded_recs"].cpu().pin_memory(), "lengths": st["lengths"].cpu().pin_memory(),
                      "samples": st["samples"].cpu().pin_memory(),
                      "qkv": st["qkv"][:wl.cap].cpu().pin_memory(), "dout": st["dout"].cpu().pin_memory()})
-    dq_host = torch.empty((wl.cap, 3, H, D), dtype=torch.bfloat16).pin_memory()
+    dq_host = [torch.empty((wl.cap, 3, H, D), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    dq_dev = [wl.dqkv, torch.empty_like(wl.dqkv)]
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    set_free = [torch.cuda.Event() for _ in range(N_SETS)]     # main stream finished with set s
+    set_ready = [torch.cuda.Event() for _ in range(N_SETS)]    # qkv/dO of set s copied in
+    dq_free = [torch.cuda.Event() for _ in range(2)]           # D2H of dq buffer i finished
     h2d = d2h = 0
 
-    def one(n):
-        nonlocal h2d, d2h
+    def load_records(n):
+        """H2D of step n's input records, lengths and sample records (side stream), then the
+        exchange's first phase (lengths all-gather)."""
+        nonlocal h2d
         s = n % N_SETS
         st, hs = wl.sets[s], host[s]
+        wl.side.wait_event(set_free[s])
         with torch.cuda.stream(wl.side):
             st["padded_recs"].copy_(hs["recs"], non_blocking=True)
             st["lengths"].copy_(hs["lengths"], non_blocking=True)
             st["samples"].copy_(hs["samples"], non_blocking=True)
-        wl.prepare(n)
-        T = wl.ex[n % 2]["T"]
-        st["qkv"][:T].copy_(hs["qkv"][:T], non_blocking=True)
-        st["dout"][:T].copy_(hs["dout"][:T], non_blocking=True)
+        wl.begin(n)
+        h2d += hs["recs"].numel() * 4 + B * 4 + B * 4
+
+    def load(n):
+        """Second phase of step n's exchange, then H2D of its qkv / dO (rows = this rank's
+        post-exchange T) on h2d_s."""
+        nonlocal h2d
+        s = n % N_SETS
+        st, hs = wl.sets[s], host[s]
+        wl.finish(n)
+        T = wl.ex[n % N_EX]["T"]
+        h2d_s.wait_event(set_free[s])
+        with torch.cuda.stream(h2d_s):
+            st["qkv"][:T].copy_(hs["qkv"][:T], non_blocking=True)
+            st["dout"][:T].copy_(hs["dout"][:T], non_blocking=True)
+        set_ready[s].record(h2d_s)
+        h2d += T * 3 * H * D * 2 + T * H * D * 2
+
+    def one(n):
+        nonlocal d2h
+        s, i = n % N_SETS, n % 2
+        T = wl.ex[n % N_EX]["T"]
+        wl.main.wait_event(set_ready[s])
+        wl.main.wait_event(dq_free[i])
+        wl.dqkv = dq_dev[i]
         _patch_lse(wl, n)
         wl.step(n)
-        dq_host[:T].copy_(wl.dqkv[:T], non_blocking=True)
-        h2d += hs["recs"].numel() * 4 + B * 4 + B * 4 + T * 3 * H * D * 2 + T * H * D * 2
+        set_free[s].record(wl.main)
+        d2h_s.wait_event(set_free[s])
+        with torch.cuda.stream(d2h_s):
+            dq_host[i][:T].copy_(dq_dev[i][:T], non_blocking=True)
+        dq_free[i].record(d2h_s)
         d2h += T * 3 * H * D * 2
+        load(n + 1)
+        load_records(n + 2)
         return T
 
     base = 10 ** 6
+    load_records(base)
+    load_records(base + 1)
+    load(base)
     for n in range(min(args.warmup, 3)):
         one(base + n)
     torch.cuda.synchronize()
     barrier(world)
+    n0 = base + min(args.warmup, 3)
     h2d = d2h = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(wl.main)
     tok = 0
     for k in range(args.steps):
-        tok += one(base + 10 + k)
+        tok += one(n0 + k)
+    # steady state: the K steps' kernels and D2H, and K H2D loads (qkv/dO of steps
+    # n0+1 .. n0+K, records of n0+2 .. n0+K+1; the earlier ones were issued in the warm-up)
+    wl.main.wait_stream(d2h_s)
+    wl.main.wait_stream(h2d_s)
+    wl.main.wait_stream(wl.side)
     e1.record(wl.main)
     torch.cuda.synchronize()
     barrier(world)
+    wl.dqkv = dq_dev[0]
+    wl.finish(n0 + args.steps + 1)              # drain the begin still in flight (untimed)
+    torch.cuda.synchronize()
     ms = all_max(e0.elapsed_time(e1), world)
     tok_all = all_sum(tok, world)
     return {"value": round(tok_all / (ms / 1e3), 1), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d // args.steps),

@@ -14,7 +14,7 @@
  *     memory; the only library-owned object is `ub_comm`.
  *   - Asynchrony: device entry points only enqueue work on `stream` and never
  *     synchronise the host (the method exists to avoid host<->device syncs).
- *     The one exception is ub_balance_exchange (documented there).
+ *     The exceptions are ub_balance_exchange / ub_exchange_finish (documented there).
  *   - Errors: arguments are validated on the host before anything is launched; on a
  *     non-OK status nothing was enqueued and ub_last_error() returns a thread-local
  *     message.  Device-resident data (cu_seqlens monotonicity, lengths <= max_seqlen)
@@ -223,6 +223,28 @@ ub_status ub_balance_exchange(void* comm, int32_t mode, int32_t B, int32_t max_s
                               int64_t capacity_tokens, void* d_out_tokens, void* d_out_samples,
                               int32_t* d_out_cu, int32_t* h_perm, int64_t* h_out_T, void* ws,
                               void* side_stream);
+
+/* The same exchange split in two so that the host never waits on work it has just
+ * enqueued (the balancing of mini-batch n+1 runs while n computes).
+ * ub_balance_exchange == ub_exchange_begin + ub_exchange_finish on an internal slot.
+ *
+ * ub_exchange_begin (device, no host wait): step 1 -- all-gather of d_my_lengths [B] into
+ *   slot `slot` (0 <= slot < UB_EXCHANGE_SLOTS) of the communicator's pinned ring, D2H on
+ *   `stream`, and an event recorded behind it.  The slot must not hold an unfinished
+ *   begin (UB_ERR_INVALID_ARG).  ws as for ub_balance_exchange (only its front is used).
+ * ub_exchange_finish: waits (host) for that slot's event only, then steps 3-7 exactly as
+ *   ub_balance_exchange on `stream`, and frees the slot.  B must equal the begin's B.
+ *   Issue the begin of step n+1 one step before its finish: by then its event has fired
+ *   and the wait is free.  Outputs, capacity and errors as ub_balance_exchange.
+ * Collective calls: every rank issues the same begin/finish sequence. */
+#define UB_EXCHANGE_SLOTS 4
+ub_status ub_exchange_begin(void* comm, int32_t slot, int32_t B, const int32_t* d_my_lengths, void* ws,
+                            void* stream);
+ub_status ub_exchange_finish(void* comm, int32_t slot, int32_t mode, int32_t B, int32_t max_seqlen,
+                             const void* d_my_tokens, const void* d_my_samples, int64_t rec_bytes,
+                             int64_t srec_bytes, int64_t capacity_tokens, void* d_out_tokens,
+                             void* d_out_samples, int32_t* d_out_cu, int32_t* h_perm, int64_t* h_out_T,
+                             void* ws, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -6,8 +6,9 @@ and backward grouped by length, and the padding-exchange load
 balancer.  The compute lives in libub.so (include/ub.h); this package is
 its argument-marshalling binding.
 """
+from ._lib import UbError
 from .api import (Comm, balance_plan, cu_seqlens, exchange_copy, exchange_tables, lengths_from_mask, pad, unpad,
                   varlen_fmha_bwd, varlen_fmha_fwd, version)
 
-__all__ = ["Comm", "balance_plan", "cu_seqlens", "exchange_copy", "exchange_tables", "lengths_from_mask", "pad",
+__all__ = ["UbError", "Comm", "balance_plan", "cu_seqlens", "exchange_copy", "exchange_tables", "lengths_from_mask", "pad",
            "unpad", "varlen_fmha_bwd", "varlen_fmha_fwd", "version"]

@@ -45,6 +45,8 @@ SIGNATURES = {
     "ub_allgather_lengths": (i32, [vp, vp, vp, i32, vp]),
     "ub_exchange_workspace_bytes": (sz, [i32, i32, i64, i64, i64]),
     "ub_balance_exchange": (i32, [vp, i32, i32, i32, vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+    "ub_exchange_begin": (i32, [vp, i32, i32, vp, vp, vp]),
+    "ub_exchange_finish": (i32, [vp, i32, i32, i32, i32, vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
 }
 
 _lib = None

@@ -220,6 +220,32 @@ class Comm:
                                         C.byref(T_out), _ptr(ws), _stream(stream)))
         return out_tokens, out_samples, out_cu, int(T_out.value), perm
 
+    SLOTS = 4    # UB_EXCHANGE_SLOTS
+
+    def _ws(self, B, capacity_tokens, rec, srec, dev):
+        return _workspace(lib().ub_exchange_workspace_bytes(self.world, B, capacity_tokens, rec, srec), dev,
+                          f"exchange{self.rank}")
+
+    def exchange_begin(self, slot: int, d_lengths, capacity_tokens, rec, srec, stream=None):
+        """Phase 1 (no host wait): all-gather of the lengths into pinned slot `slot`."""
+        ws = self._ws(d_lengths.numel(), capacity_tokens, rec, srec, d_lengths.device)
+        check(lib().ub_exchange_begin(self.handle, int(slot), d_lengths.numel(), _ptr(d_lengths), _ptr(ws),
+                                      _stream(stream)))
+
+    def exchange_finish(self, slot: int, B, d_tokens, d_samples, capacity_tokens, max_seqlen, mode, out_tokens,
+                        out_samples, out_cu, stream=None):
+        """Phase 2: plan, pack, all-to-all-v, unpack; returns (T_out, perm)."""
+        rec = int(np.prod(d_tokens.shape[1:])) * d_tokens.element_size()
+        srec = int(np.prod(d_samples.shape[1:])) * d_samples.element_size() if d_samples is not None else 0
+        ws = self._ws(B, capacity_tokens, rec, srec, out_tokens.device)
+        perm = np.zeros(self.world * B, dtype=np.int32)
+        T_out = C.c_int64(0)
+        check(lib().ub_exchange_finish(self.handle, int(slot), BAL_MODES[mode], B, int(max_seqlen), _ptr(d_tokens),
+                                       _ptr(d_samples), rec, srec, int(capacity_tokens), _ptr(out_tokens),
+                                       _ptr(out_samples), _ptr(out_cu), _np_ptr(perm), C.byref(T_out), _ptr(ws),
+                                       _stream(stream)))
+        return int(T_out.value), perm
+
     def close(self):
         if self.handle:
             check(lib().ub_comm_destroy(self.handle))

@@ -8,6 +8,9 @@
 // step n+1's exchange overlaps step n's compute.
 #include <nccl.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -15,17 +18,31 @@
 
 namespace ub {
 
+constexpr int32_t kExSlots = UB_EXCHANGE_SLOTS + 1;  // the last one serves ub_balance_exchange
+
 struct Comm {
   ncclComm_t nccl = nullptr;
   int32_t W = 0, rank = 0;
-  // pinned host staging (reused across calls; every call synchronises the side stream
-  // before rewriting it)
+  // pinned host staging.  h_all: kExSlots rings of W*cap_B lengths, each filled by a begin
+  // and guarded by ev_len[slot].  The plan tables / cu are rewritten by every finish only
+  // after ev_staging (behind the previous finish's H2D copies) has fired.
   int32_t* h_all = nullptr;
   int64_t* h_tab_pack = nullptr;
   int64_t* h_tab_unpack = nullptr;
   int32_t* h_cu = nullptr;
   int32_t cap_B = 0;
+  int32_t slot_B[kExSlots] = {};      // B of the pending begin, 0 = free
+  cudaEvent_t ev_len[kExSlots] = {};
+  cudaEvent_t ev_staging = nullptr;
+  // UB_EXCHANGE_TRACE=1: host time per finish phase, printed at ub_comm_destroy (dev aid)
+  bool trace = false;
+  double t_phase[8] = {};
+  int64_t n_finish = 0;
 };
+
+static double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 #define UB_CHECK_NCCL(expr)                                                                  \
   do {                                                                                       \
@@ -34,17 +51,38 @@ struct Comm {
       return ::ub::set_error(UB_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_));          \
   } while (0)
 
-static ub_status ensure_staging(Comm* c, int32_t B) {
-  if (c->cap_B >= B) return UB_OK;
+static void free_staging(Comm* c) {
   cudaFreeHost(c->h_all);
   cudaFreeHost(c->h_tab_pack);
   cudaFreeHost(c->h_tab_unpack);
   cudaFreeHost(c->h_cu);
   c->h_all = nullptr; c->h_tab_pack = nullptr; c->h_tab_unpack = nullptr; c->h_cu = nullptr; c->cap_B = 0;
-  UB_CHECK_CUDA(cudaMallocHost(&c->h_all, sizeof(int32_t) * (size_t)c->W * B));
+}
+
+static ub_status ensure_staging(Comm* c, int32_t B) {
+  if (!c->ev_staging) {
+    for (auto& e : c->ev_len) UB_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    UB_CHECK_CUDA(cudaEventCreateWithFlags(&c->ev_staging, cudaEventDisableTiming));
+  }
+  if (c->cap_B >= B) return UB_OK;
+  // growing: wait for every pending copy into / out of the old buffers, keep pending slots
+  for (auto& e : c->ev_len) UB_CHECK_CUDA(cudaEventSynchronize(e));
+  UB_CHECK_CUDA(cudaEventSynchronize(c->ev_staging));
+  int32_t* old_all = c->h_all;
+  const int32_t old_cap = c->cap_B;
+  c->h_all = nullptr;
+  free_staging(c);
+  UB_CHECK_CUDA(cudaMallocHost(&c->h_all, sizeof(int32_t) * (size_t)kExSlots * c->W * B));
   UB_CHECK_CUDA(cudaMallocHost(&c->h_tab_pack, sizeof(int64_t) * 5 * (size_t)B));
   UB_CHECK_CUDA(cudaMallocHost(&c->h_tab_unpack, sizeof(int64_t) * 5 * (size_t)B));
   UB_CHECK_CUDA(cudaMallocHost(&c->h_cu, sizeof(int32_t) * ((size_t)B + 1)));
+  if (old_all) {
+    for (int32_t k = 0; k < kExSlots; ++k)
+      if (c->slot_B[k])
+        std::memcpy(c->h_all + (size_t)k * c->W * B, old_all + (size_t)k * c->W * old_cap,
+                    sizeof(int32_t) * (size_t)c->W * c->slot_B[k]);
+    cudaFreeHost(old_all);
+  }
   c->cap_B = B;
   return UB_OK;
 }
@@ -56,7 +94,7 @@ struct ExWs {  // carve-up of the exchange workspace
 static size_t ex_layout(int32_t W, int32_t B, int64_t cap, int64_t rec, int64_t srec, void* base, ExWs* out) {
   size_t off = 0;
   auto take = [&](size_t n) { size_t o = off; off = align_up(off + n, 256); return o; };
-  const size_t o_all = take(sizeof(int32_t) * (size_t)W * B);
+  const size_t o_all = take(sizeof(int32_t) * (size_t)kExSlots * W * B);  // one gather target per slot
   const size_t o_tp = take(sizeof(int64_t) * 5 * (size_t)B);
   const size_t o_tu = take(sizeof(int64_t) * 5 * (size_t)B);
   const size_t o_st = take((size_t)cap * rec);
@@ -97,6 +135,8 @@ extern "C" ub_status ub_comm_init(void** out_comm, const void* id_128, int32_t W
   ncclUniqueId id;
   std::memcpy(&id, id_128, sizeof(id));
   Comm* c = new Comm();
+  const char* tr = std::getenv("UB_EXCHANGE_TRACE");
+  c->trace = tr && tr[0] == '1';
   c->W = W;
   c->rank = rank;
   ncclResult_t r = ncclCommInitRank(&c->nccl, W, id, rank);
@@ -112,11 +152,21 @@ extern "C" ub_status ub_comm_destroy(void* comm) {
   clear_error();
   if (!comm) return UB_OK;
   Comm* c = static_cast<Comm*>(comm);
+  if (c->trace && c->n_finish) {
+    static const char* names[] = {"wait_lengths", "plan", "wait_staging", "tables", "pack", "nccl_p2p", "unpack_cu"};
+    std::fprintf(stderr, "[ub exchange trace] rank %d, %lld finishes, host us per finish:", c->rank,
+                 (long long)c->n_finish);
+    for (int k = 0; k < 7; ++k) std::fprintf(stderr, " %s=%.1f", names[k], c->t_phase[k] / c->n_finish);
+    std::fprintf(stderr, "\n");
+  }
+  for (auto e : c->ev_len)
+    if (e) cudaEventSynchronize(e);
+  if (c->ev_staging) cudaEventSynchronize(c->ev_staging);
   if (c->nccl) ncclCommDestroy(c->nccl);
-  cudaFreeHost(c->h_all);
-  cudaFreeHost(c->h_tab_pack);
-  cudaFreeHost(c->h_tab_unpack);
-  cudaFreeHost(c->h_cu);
+  free_staging(c);
+  for (auto e : c->ev_len)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_staging) cudaEventDestroy(c->ev_staging);
   delete c;
   return UB_OK;
 }
@@ -134,72 +184,166 @@ extern "C" size_t ub_exchange_workspace_bytes(int32_t W, int32_t B, int64_t cap,
   return ex_layout(W, B, cap, rec, srec, nullptr, nullptr);
 }
 
-extern "C" ub_status ub_balance_exchange(void* comm, int32_t mode, int32_t B, int32_t max_seqlen,
-                                         const int32_t* d_my_lengths, const void* d_my_tokens,
-                                         const void* d_my_samples, int64_t rec, int64_t srec, int64_t cap,
-                                         void* d_out_tokens, void* d_out_samples, int32_t* d_out_cu,
-                                         int32_t* h_perm, int64_t* h_out_T, void* ws, void* side_stream) {
-  clear_error();
-  UB_REQUIRE(comm && d_my_lengths && d_my_tokens && d_out_tokens && d_out_cu && h_out_T && ws, UB_ERR_INVALID_ARG,
-             "null pointer");
-  UB_REQUIRE(B >= 1 && rec > 0 && srec >= 0 && cap >= 1, UB_ERR_SHAPE, "bad sizes");
-  UB_REQUIRE(srec == 0 || (d_my_samples && d_out_samples), UB_ERR_INVALID_ARG, "null sample pointer");
-  Comm* c = static_cast<Comm*>(comm);
-  const int32_t W = c->W, me = c->rank;
-  cudaStream_t s = as_stream(side_stream);
+static ub_status exchange_begin(Comm* c, int32_t slot, int32_t B, const int32_t* d_my_lengths, void* ws,
+                                cudaStream_t s) {
+  UB_REQUIRE(c->slot_B[slot] == 0, UB_ERR_INVALID_ARG, "exchange slot %d already holds an unfinished begin", slot);
   ub_status st = ensure_staging(c, B);
   if (st != UB_OK) return st;
+  const size_t n = (size_t)c->W * B;
+  int32_t* d_all = static_cast<int32_t*>(ws) + (size_t)slot * n;   // ex_layout: lengths at the front
+  // 1. all-gather of lengths (P:355 step 1, lengths only), 2. D2H into the pinned ring
+  // (one rank: the gather is the identity, no collective)
+  if (c->W > 1) UB_CHECK_NCCL(ncclAllGather(d_my_lengths, d_all, (size_t)B, ncclInt32, c->nccl, s));
+  UB_CHECK_CUDA(cudaMemcpyAsync(c->h_all + (size_t)slot * c->W * c->cap_B, c->W > 1 ? d_all : d_my_lengths,
+                                sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  UB_CHECK_CUDA(cudaEventRecord(c->ev_len[slot], s));
+  c->slot_B[slot] = B;
+  return UB_OK;
+}
+
+static ub_status exchange_finish(Comm* c, int32_t slot, int32_t mode, int32_t B, int32_t max_seqlen,
+                                 const void* d_my_tokens, const void* d_my_samples, int64_t rec, int64_t srec,
+                                 int64_t cap, void* d_out_tokens, void* d_out_samples, int32_t* d_out_cu,
+                                 int32_t* h_perm, int64_t* h_out_T, void* ws, cudaStream_t s) {
+  UB_REQUIRE(c->slot_B[slot] == B, UB_ERR_INVALID_ARG, "exchange slot %d: no begin with B=%d pending", slot, B);
+  const int32_t W = c->W, me = c->rank;
   ExWs w;
   ex_layout(W, B, cap, rec, srec, ws, &w);
-
-  // 1. all-gather of lengths (P:355 step 1, lengths only)
-  UB_CHECK_NCCL(ncclAllGather(d_my_lengths, w.all_lengths, (size_t)B, ncclInt32, c->nccl, s));
-  // 2. lengths to the host: the single host wait, on the side stream only
-  UB_CHECK_CUDA(cudaMemcpyAsync(c->h_all, w.all_lengths, sizeof(int32_t) * (size_t)W * B, cudaMemcpyDeviceToHost, s));
-  UB_CHECK_CUDA(cudaStreamSynchronize(s));
+  double tp[9];
+  int ip = 0;
+  if (c->trace) tp[ip++] = now_us();
+#define UB_PHASE() do { if (c->trace) tp[ip++] = now_us(); } while (0)
+  // the single host wait: this slot's lengths (enqueued by the begin, normally long done)
+  UB_CHECK_CUDA(cudaEventSynchronize(c->ev_len[slot]));
+  UB_PHASE();
+  c->slot_B[slot] = 0;
+  const int32_t* h_all = c->h_all + (size_t)slot * W * c->cap_B;
   // 3. the deterministic plan, identical on every rank
   std::vector<int32_t> perm((size_t)W * B);
-  if ((st = ub_balance_plan(c->h_all, W, B, max_seqlen, mode, perm.data(), nullptr, nullptr, nullptr)) != UB_OK)
+  ub_status st;
+  if ((st = ub_balance_plan(h_all, W, B, max_seqlen, mode, perm.data(), nullptr, nullptr, nullptr)) != UB_OK)
     return st;
+  UB_PHASE();
+  // the previous finish's H2D copies out of the staging buffers must have completed
+  UB_CHECK_CUDA(cudaEventSynchronize(c->ev_staging));
+  UB_PHASE();
   std::vector<int64_t> send_cnt(W), send_scnt(W), recv_cnt(W), recv_scnt(W);
   int64_t T_mine = 0, T_out = 0;
-  if ((st = ub_exchange_tables(c->h_all, perm.data(), W, B, me, 0, c->h_tab_pack, send_cnt.data(), send_scnt.data(),
+  if ((st = ub_exchange_tables(h_all, perm.data(), W, B, me, 0, c->h_tab_pack, send_cnt.data(), send_scnt.data(),
                                &T_mine)) != UB_OK)
     return st;
-  if ((st = ub_exchange_tables(c->h_all, perm.data(), W, B, me, 1, c->h_tab_unpack, recv_cnt.data(),
-                               recv_scnt.data(), &T_out)) != UB_OK)
+  if ((st = ub_exchange_tables(h_all, perm.data(), W, B, me, 1, c->h_tab_unpack, recv_cnt.data(), recv_scnt.data(),
+                               &T_out)) != UB_OK)
     return st;
   UB_REQUIRE(T_mine <= cap && T_out <= cap, UB_ERR_CAPACITY, "tokens (%lld sent, %lld received) exceed capacity %lld",
              (long long)T_mine, (long long)T_out, (long long)cap);
+  UB_PHASE();
   // 4. pack into destination order
   UB_CHECK_CUDA(cudaMemcpyAsync(w.tab_pack, c->h_tab_pack, sizeof(int64_t) * 5 * B, cudaMemcpyHostToDevice, s));
   UB_CHECK_CUDA(cudaMemcpyAsync(w.tab_unpack, c->h_tab_unpack, sizeof(int64_t) * 5 * B, cudaMemcpyHostToDevice, s));
   if ((st = ub_exchange_copy(d_my_tokens, w.send_tok, d_my_samples, w.send_smp, w.tab_pack, B, rec, srec, s)) != UB_OK)
     return st;
-  // 5. all-to-all-v over NVLink (grouped point-to-point)
-  UB_CHECK_NCCL(ncclGroupStart());
+  UB_PHASE();
+  // 5. all-to-all-v over NVLink (grouped point-to-point); the chunk a rank keeps is a
+  // device copy, so one rank issues no collective at all
   int64_t so = 0, ro = 0, sso = 0, rso = 0;
+  bool any_peer = false;
   for (int32_t peer = 0; peer < W; ++peer) {
-    if (send_cnt[peer] > 0)
-      UB_CHECK_NCCL(ncclSend(w.send_tok + so * rec, (size_t)(send_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
-    if (recv_cnt[peer] > 0)
-      UB_CHECK_NCCL(ncclRecv(w.recv_tok + ro * rec, (size_t)(recv_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
-    if (srec > 0 && send_scnt[peer] > 0)
-      UB_CHECK_NCCL(ncclSend(w.send_smp + sso * srec, (size_t)(send_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
-    if (srec > 0 && recv_scnt[peer] > 0)
-      UB_CHECK_NCCL(ncclRecv(w.recv_smp + rso * srec, (size_t)(recv_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
+    if (peer == me) {
+      UB_REQUIRE(send_cnt[me] == recv_cnt[me] && send_scnt[me] == recv_scnt[me], UB_ERR_INVALID_ARG,
+                 "exchange tables disagree on the self chunk");
+      if (send_cnt[me] > 0)
+        UB_CHECK_CUDA(cudaMemcpyAsync(w.recv_tok + ro * rec, w.send_tok + so * rec, (size_t)(send_cnt[me] * rec),
+                                      cudaMemcpyDeviceToDevice, s));
+      if (srec > 0 && send_scnt[me] > 0)
+        UB_CHECK_CUDA(cudaMemcpyAsync(w.recv_smp + rso * srec, w.send_smp + sso * srec,
+                                      (size_t)(send_scnt[me] * srec), cudaMemcpyDeviceToDevice, s));
+    } else {
+      any_peer = any_peer || send_cnt[peer] > 0 || recv_cnt[peer] > 0 || send_scnt[peer] > 0 || recv_scnt[peer] > 0;
+    }
     so += send_cnt[peer]; ro += recv_cnt[peer]; sso += send_scnt[peer]; rso += recv_scnt[peer];
   }
-  UB_CHECK_NCCL(ncclGroupEnd());
+  if (any_peer) {
+    UB_CHECK_NCCL(ncclGroupStart());
+    so = ro = sso = rso = 0;
+    for (int32_t peer = 0; peer < W; ++peer) {
+      if (peer != me) {
+        if (send_cnt[peer] > 0)
+          UB_CHECK_NCCL(ncclSend(w.send_tok + so * rec, (size_t)(send_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
+        if (recv_cnt[peer] > 0)
+          UB_CHECK_NCCL(ncclRecv(w.recv_tok + ro * rec, (size_t)(recv_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
+        if (srec > 0 && send_scnt[peer] > 0)
+          UB_CHECK_NCCL(
+              ncclSend(w.send_smp + sso * srec, (size_t)(send_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
+        if (srec > 0 && recv_scnt[peer] > 0)
+          UB_CHECK_NCCL(
+              ncclRecv(w.recv_smp + rso * srec, (size_t)(recv_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
+      }
+      so += send_cnt[peer]; ro += recv_cnt[peer]; sso += send_scnt[peer]; rso += recv_scnt[peer];
+    }
+    UB_CHECK_NCCL(ncclGroupEnd());
+  }
+  UB_PHASE();
   // 6. reorder the per-source chunks into perm order (a5)
   if ((st = ub_exchange_copy(w.recv_tok, d_out_tokens, w.recv_smp, d_out_samples, w.tab_unpack, B, rec, srec, s)) !=
       UB_OK)
     return st;
   // 7. the new cu_seqlens, computed on the host (input-only operators run during the exchange)
   c->h_cu[0] = 0;
-  for (int32_t k = 0; k < B; ++k) c->h_cu[k + 1] = c->h_cu[k] + c->h_all[perm[(size_t)me * B + k]];
+  for (int32_t k = 0; k < B; ++k) c->h_cu[k + 1] = c->h_cu[k] + h_all[perm[(size_t)me * B + k]];
   UB_CHECK_CUDA(cudaMemcpyAsync(d_out_cu, c->h_cu, sizeof(int32_t) * (B + 1), cudaMemcpyHostToDevice, s));
+  UB_CHECK_CUDA(cudaEventRecord(c->ev_staging, s));
+  UB_PHASE();
+#undef UB_PHASE
+  if (c->trace) {
+    for (int k = 1; k < ip && k < 9; ++k) c->t_phase[k - 1] += tp[k] - tp[k - 1];
+    ++c->n_finish;
+  }
   if (h_perm) std::memcpy(h_perm, perm.data(), sizeof(int32_t) * perm.size());
   *h_out_T = T_out;
   return UB_OK;
+}
+
+#define UB_EXCHANGE_ARGS_CHECK()                                                                            \
+  UB_REQUIRE(comm && d_my_tokens && d_out_tokens && d_out_cu && h_out_T && ws, UB_ERR_INVALID_ARG, "null pointer"); \
+  UB_REQUIRE(B >= 1 && rec > 0 && srec >= 0 && cap >= 1, UB_ERR_SHAPE, "bad sizes");                        \
+  UB_REQUIRE(srec == 0 || (d_my_samples && d_out_samples), UB_ERR_INVALID_ARG, "null sample pointer")
+
+extern "C" ub_status ub_exchange_begin(void* comm, int32_t slot, int32_t B, const int32_t* d_my_lengths, void* ws,
+                                       void* stream) {
+  clear_error();
+  UB_REQUIRE(comm && d_my_lengths && ws, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(B >= 1, UB_ERR_SHAPE, "B must be >= 1");
+  UB_REQUIRE(slot >= 0 && slot < UB_EXCHANGE_SLOTS, UB_ERR_INVALID_ARG, "slot %d out of [0, %d)", slot,
+             UB_EXCHANGE_SLOTS);
+  return exchange_begin(static_cast<Comm*>(comm), slot, B, d_my_lengths, ws, as_stream(stream));
+}
+
+extern "C" ub_status ub_exchange_finish(void* comm, int32_t slot, int32_t mode, int32_t B, int32_t max_seqlen,
+                                        const void* d_my_tokens, const void* d_my_samples, int64_t rec, int64_t srec,
+                                        int64_t cap, void* d_out_tokens, void* d_out_samples, int32_t* d_out_cu,
+                                        int32_t* h_perm, int64_t* h_out_T, void* ws, void* stream) {
+  clear_error();
+  UB_EXCHANGE_ARGS_CHECK();
+  UB_REQUIRE(slot >= 0 && slot < UB_EXCHANGE_SLOTS, UB_ERR_INVALID_ARG, "slot %d out of [0, %d)", slot,
+             UB_EXCHANGE_SLOTS);
+  return exchange_finish(static_cast<Comm*>(comm), slot, mode, B, max_seqlen, d_my_tokens, d_my_samples, rec, srec,
+                         cap, d_out_tokens, d_out_samples, d_out_cu, h_perm, h_out_T, ws, as_stream(stream));
+}
+
+extern "C" ub_status ub_balance_exchange(void* comm, int32_t mode, int32_t B, int32_t max_seqlen,
+                                         const int32_t* d_my_lengths, const void* d_my_tokens,
+                                         const void* d_my_samples, int64_t rec, int64_t srec, int64_t cap,
+                                         void* d_out_tokens, void* d_out_samples, int32_t* d_out_cu,
+                                         int32_t* h_perm, int64_t* h_out_T, void* ws, void* side_stream) {
+  clear_error();
+  UB_EXCHANGE_ARGS_CHECK();
+  UB_REQUIRE(d_my_lengths, UB_ERR_INVALID_ARG, "null pointer");
+  Comm* c = static_cast<Comm*>(comm);
+  cudaStream_t s = as_stream(side_stream);
+  const int32_t slot = kExSlots - 1;
+  ub_status st = exchange_begin(c, slot, B, d_my_lengths, ws, s);
+  if (st != UB_OK) return st;
+  return exchange_finish(c, slot, mode, B, max_seqlen, d_my_tokens, d_my_samples, rec, srec, cap, d_out_tokens,
+                         d_out_samples, d_out_cu, h_perm, h_out_T, ws, s);
 }

@@ -13,20 +13,26 @@
 // P~^T and dS^T are already the A operands of dV and dK and never leave TMEM (TS MMA); only
 // dS goes to smem, for dQ.
 //
-// CTA = 10 warps (1 per SM):
-//   warps 0-7  two compute warpgroups: thread r of warpgroup x owns key row r and query
-//              columns [64x, 64x+64) of S^T / dP^T; it also stages its half of dQ
-//   warp 8     producer: K, V per item (double-buffered) and Q, dO per query tile (2 stages)
-//              by TMA; the tile's LSE / Delta vectors by the 32 lanes into smem
-//   warp 9     TMEM allocator, then MMA issuer (one thread)
+// CTA = 16 warps (1 per SM), four warpgroups:
+//   warps 0-7   two compute warpgroups: thread r of warpgroup x owns key row r and query
+//               columns [64x, 64x+64) of S^T / dP^T
+//   warps 8-11  epilogue warpgroup: dQ_i out of TMEM into the fp32 accumulator, and dK / dV
+//               of the finished item, so the compute warps never leave the exp/dS loop
+//   warp 12     producer of Q, dO per query tile (2 stages) by TMA; the tile's LSE / Delta
+//               vectors by the 32 lanes into smem
+//   warp 13     TMEM allocator, then MMA issuer (one thread)
+//   warp 14     producer of K, V per item (double-buffered); warp 15 idle
+// Registers: 128 per thread at launch; setmaxnreg moves them to the compute warpgroups
+// (168) from the others (88): per SMSP 2 x 168 + 2 x 88 = 512 = 4 x 128.
 // TMEM columns: S^T 0..127, dP^T 128..255, P~^T 256..319 (bf16 pairs), dS^T 320..383
 // (bf16 pairs; dQ_i = dS K is written over it after dK_i has read it -- tcgen05.mma ops of
 // one thread execute in issue order), dV 384..447, dK 448..511.
 // The MMA issues S_{i+1}, dP_{i+1} as soon as the compute warps have loaded S_i, dP_i, so
-// the exp/dS phase of tile i overlaps the tensor work of tile i+1.
+// the exp/dS phase of tile i overlaps the tensor work of tile i+1; the compute warps write
+// P~_{i+1} / dS_{i+1} once the epilogue has read dQ_i out (which implies grads_i are done).
 // dQ_i leaves through per-warp smem staging (128-B swizzle) and cp.reduce.async.bulk.tensor
-// add into an fp32 [H*T, 64] accumulator (one TMA op per warp instead of 8192 atomics);
-// dK / dV of whole warps leave by TMA store from the same staging (64-B swizzle).
+// add into an fp32 [H*T, 64] accumulator (two TMA ops per warp instead of 8192 atomics);
+// dK / dV of whole warps leave by TMA store from the same staging.
 #include <cmath>
 
 #include "fmha_common.cuh"
@@ -35,7 +41,7 @@ namespace ub {
 namespace bwd {
 
 #ifdef UB_TRACE
-__device__ uint64_t g_trace[10 * 1024];
+__device__ uint64_t g_trace[16 * 1024];
 #define TR(ev)                                                                                          \
   do {                                                                                                  \
     if (blockIdx.x == 0 && lane == 0 && tr_n < 1024)                                                    \
@@ -48,21 +54,23 @@ __device__ uint64_t g_trace[10 * 1024];
 constexpr int kD = 64;
 constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
 constexpr uint32_t kPBytes = kTile * kTile * 2;   // 32 KB
-constexpr int kThreads = 320;
+constexpr int kThreads = 512;
+constexpr uint32_t kQStages = 3;                  // Q / dO / LSE / Delta pipeline depth
 constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDS = 320, kColDQ = 320, kColDV = 384, kColDK = 448;
 
 struct Smem {
   uint8_t k[2][kTileBytes];
   uint8_t v[2][kTileBytes];
-  uint8_t q[2][kTileBytes];
-  uint8_t dO[2][kTileBytes];
+  uint8_t q[kQStages][kTileBytes];
+  uint8_t dO[kQStages][kTileBytes];
   uint8_t ds[kPBytes];              // dS^T [key][query], 2 x 64-query SW128 regions
-  uint8_t dq[2][kTile * 128];       // dQ staging per warpgroup: [128 rows][32 fp32] SW128
-  float lse[2][kTile];              // LSE of the query tile's rows (natural log)
-  float delta[2][kTile];
+  uint8_t stage[4][4096];           // per epilogue warp: [32 rows][128 B], 128-B swizzle: half of
+                                    // dQ (32 fp32 columns), or dK, or dV (64 bf16)
+  float lse[kQStages][kTile];       // LSE of the query tile's rows (natural log)
+  float delta[kQStages][kTile];
   uint64_t kv_full[2], kv_empty[2];
-  uint64_t qdo_full[2], qdo_empty[2];
-  uint64_t s_full, s_free, pds_full, pds_empty, dkv_full, dkv_free;
+  uint64_t qdo_full[kQStages], qdo_empty[kQStages];
+  uint64_t s_full, s_free, pds_full, dq_full, dq_empty, dkv_full, dkv_free;
   uint32_t tmem_base;
   PlanSmem plan;
 };
@@ -116,7 +124,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   uint32_t tr_n = 0;
   (void)tr_n;
 
-  if (warp == 8 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
     tma_prefetch_desc(&tmap_do);
     tma_prefetch_desc(&tmap_dq);
@@ -124,33 +132,41 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.kv_full[s], 1);
       mbar_init(&sm.kv_empty[s], 1);
+    }
+    for (uint32_t s = 0; s < kQStages; ++s) {
       mbar_init(&sm.qdo_full[s], 1);
       mbar_init(&sm.qdo_empty[s], 1);
     }
     mbar_init(&sm.s_full, 1);
     mbar_init(&sm.s_free, 8);
     mbar_init(&sm.pds_full, 8);
-    mbar_init(&sm.pds_empty, 1);
+    mbar_init(&sm.dq_full, 1);
+    mbar_init(&sm.dq_empty, 4);
     mbar_init(&sm.dkv_full, 1);
-    mbar_init(&sm.dkv_free, 8);
+    mbar_init(&sm.dkv_free, 4);
     fence_mbar_init();
   }
-  if (!kBigB && warp == 8) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 1, lane);
-  if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
+  if (!kBigB && warp == 12) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 1, lane);
+  if (warp == 13) tmem_alloc(&sm.tmem_base, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const int32_t H = prm.H;
+  // each role re-sizes its registers at its entry, inside its branch (ptxas takes the
+  // minimum where paths merge); setmaxnreg is warpgroup-uniform
 
-  if (warp == 8) {
-    // ------------------------------------------------------------ producer
-    uint32_t items = 0, qit = 0;
-    WorkItem it;
-    for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it);
-         w += gridDim.x, ++items) {
-      const uint32_t kvs = items & 1;
-      if (lane == 0) {
+  if (warp >= 12) {
+    regs_dec<88>();
+  }
+  if (warp == 14) {
+    // ------------------------------------------------------------ K / V producer (per item)
+    if (lane == 0) {
+      uint32_t items = 0;
+      WorkItem it;
+      for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it);
+           w += gridDim.x, ++items) {
+        const uint32_t kvs = items & 1;
         TR(20);
         mbar_wait(&sm.kv_empty[kvs], ((items >> 1) & 1) ^ 1);
         TR(21);
@@ -159,8 +175,15 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         tma_load_2d(sm.k[kvs], &tmap_qkv, &sm.kv_full[kvs], (H + it.h) * kD, krow);
         tma_load_2d(sm.v[kvs], &tmap_qkv, &sm.kv_full[kvs], (2 * H + it.h) * kD, krow);
       }
+    }
+  } else if (warp == 12) {
+    // ------------------------------------------------------------ Q / dO producer (per pair)
+    uint32_t qit = 0;
+    WorkItem it;
+    for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it);
+         w += gridDim.x) {
       for (int32_t i = 0; i < it.nt; ++i, ++qit) {
-        const uint32_t st = qit & 1;
+        const uint32_t st = qit % kQStages, ph = (qit / kQStages) & 1;
         const int32_t q0 = it.c0 + i * kTile;
         // LSE / Delta loads are issued before the stage wait so their latency hides behind it
         float lv[4], dv[4];
@@ -173,7 +196,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           dv[u] = ok ? __ldg(prm.delta + idx) : 0.f;
         }
         TR(22);
-        mbar_wait(&sm.qdo_empty[st], ((qit >> 1) & 1) ^ 1);
+        mbar_wait(&sm.qdo_empty[st], ph ^ 1);
         TR(23);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -193,11 +216,42 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         __syncwarp();
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 13) {
     // ------------------------------------------------------------ MMA issuer
+    // One pipeline over all (item, query tile) pairs: S_p, dP_p are issued before the grads of
+    // pair p-1, also across item boundaries, so the compute warps never wait for the previous
+    // item's last grads before they can start on the next item.
     if (lane == 0) {
       uint32_t items = 0, qit = 0, s_cnt = 0, g_cnt = 0;
       const uint32_t ds_addr = smem_u32(sm.ds);
+      bool pend = false, p_first = false, p_last = false;    // the pair whose grads are pending
+      uint32_t p_st = 0, p_kaddr = 0, p_kvs = 0, p_item = 0;
+      auto grads = [&]() {
+        mbar_wait(&sm.pds_full, g_cnt & 1);
+        if (p_first) mbar_wait(&sm.dkv_free, (p_item & 1) ^ 1);
+        TR(12);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(sm.q[p_st]), do_addr = smem_u32(sm.dO[p_st]);
+#pragma unroll
+        for (uint32_t k = 0; k < kTile / 16; ++k)        // K = query rows, 16 per MMA
+          umma_bf16_ts(tmem + kColDV, tmem + kColP + k * 8, sdesc_sw128(do_addr + k * 2048, 8192, 1024), kIdescTS,
+                       (p_first && k == 0) ? 0u : 1u);
+#pragma unroll
+        for (uint32_t k = 0; k < kTile / 16; ++k)
+          umma_bf16_ts(tmem + kColDK, tmem + kColDS + k * 8, sdesc_sw128(q_addr + k * 2048, 8192, 1024), kIdescTS,
+                       (p_first && k == 0) ? 0u : 1u);
+        umma_commit(&sm.qdo_empty[p_st]);              // Q_i / dO_i no longer needed
+#pragma unroll
+        for (uint32_t k = 0; k < kTile / 16; ++k)        // K = key rows, 16 per MMA
+          umma_bf16_ss(tmem + kColDQ, sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024),
+                       sdesc_sw128(p_kaddr + k * 2048, 8192, 1024), kIdescQ, k > 0);
+        umma_commit(&sm.dq_full);                      // grads_i done; dQ_i in TMEM
+        ++g_cnt;
+        if (p_last) {                                  // the item's K, V and dK, dV are final
+          umma_commit(&sm.kv_empty[p_kvs]);
+          umma_commit(&sm.dkv_full);
+        }
+      };
       WorkItem it;
       for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
         const uint32_t kvs = items & 1;
@@ -205,32 +259,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         TR(16);
         mbar_wait(&sm.kv_full[kvs], (items >> 1) & 1);
         TR(17);
-        auto grads = [&](uint32_t st, bool first) {
-          mbar_wait(&sm.pds_full, g_cnt & 1);
-          if (first) mbar_wait(&sm.dkv_free, (items & 1) ^ 1);
-          TR(12);
-          tc_fence_after();
-          const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
-#pragma unroll
-          for (uint32_t k = 0; k < kTile / 16; ++k)        // K = query rows, 16 per MMA
-            umma_bf16_ts(tmem + kColDV, tmem + kColP + k * 8, sdesc_sw128(do_addr + k * 2048, 8192, 1024), kIdescTS,
-                         (first && k == 0) ? 0u : 1u);
-#pragma unroll
-          for (uint32_t k = 0; k < kTile / 16; ++k)
-            umma_bf16_ts(tmem + kColDK, tmem + kColDS + k * 8, sdesc_sw128(q_addr + k * 2048, 8192, 1024), kIdescTS,
-                         (first && k == 0) ? 0u : 1u);
-          umma_commit(&sm.qdo_empty[st]);                // Q_i / dO_i no longer needed
-#pragma unroll
-          for (uint32_t k = 0; k < kTile / 16; ++k)        // K = key rows, 16 per MMA
-            umma_bf16_ss(tmem + kColDQ, sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024),
-                         sdesc_sw128(k_addr + k * 2048, 8192, 1024), kIdescQ, k > 0);
-          umma_commit(&sm.pds_empty);
-          ++g_cnt;
-        };
-        uint32_t prev_st = 0;
         for (int32_t i = 0; i < it.nt; ++i, ++qit) {
-          const uint32_t st = qit & 1;
-          mbar_wait(&sm.qdo_full[st], (qit >> 1) & 1);
+          const uint32_t st = qit % kQStages;
+          mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);
           TR(18);
           mbar_wait(&sm.s_free, (s_cnt & 1) ^ 1);
           TR(10);
@@ -245,16 +276,18 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           }
           umma_commit(&sm.s_full);
           ++s_cnt;
-          if (i > 0) grads(prev_st, i == 1);
-          prev_st = st;
+          if (pend) grads();
+          pend = true;
+          p_st = st; p_kaddr = k_addr; p_kvs = kvs; p_item = items;
+          p_first = i == 0;
+          p_last = i == it.nt - 1;
         }
-        grads(prev_st, it.nt == 1);
-        umma_commit(&sm.kv_empty[kvs]);
-        umma_commit(&sm.dkv_full);
       }
+      if (pend) grads();
     }
-  } else {
+  } else if (warp < 8) {
     // ------------------------------------------------------------ compute warpgroups
+    regs_inc<168>();
     const uint32_t x = warp >> 2;                           // query-column half
     const uint32_t r = threadIdx.x & 127u;                  // key row (TMEM lane)
     const uint32_t t_row = tmem + (((warp & 3) * 32) << 16);
@@ -262,47 +295,18 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     const uint64_t c2 = f2pack(c, c);
     const uint64_t nl2e2 = f2pack(-1.4426950408889634f, -1.4426950408889634f);
     const uint32_t ds_addr = smem_u32(sm.ds) + x * (kTile * 128);
-    const uint32_t dq_addr = smem_u32(sm.dq[x]);
     uint32_t s_cnt = 0, g_cnt = 0, qit = 0, items = 0;
-    bool has_prev = false;
-    int32_t prev_row0 = 0;                                  // dQ accumulator row of the pending tile
     WorkItem it;
-
-    // per-warp staging slice (32 rows x 128 B) of the warpgroup's dQ buffer; every warp
-    // moves its own rows, so no cross-warp barrier is needed
-    const uint32_t lr = r & 31u;
-    uint8_t* stage = sm.dq[x] + (warp & 3) * 4096;
-    const uint32_t stage_addr = smem_u32(stage);
-    auto stage_free = [&]() {                               // this warp's previous bulk op read it
-      if (lane == 0) bulk_wait_group_read0();
-      __syncwarp();
-    };
-    auto dq_epilogue = [&](int32_t row0) {
-      // pds_empty (waited by the caller) means dQ of the previous tile sits in TMEM
-      uint32_t d[32];
-      tmem_ld32(t_row + kColDQ + x * 32, d);
-      tmem_ld_wait();
-      stage_free();
-#pragma unroll
-      for (int g = 0; g < 8; ++g)
-        st_shared_v4(stage_addr + sw128_off(lr, g), d[4 * g], d[4 * g + 1], d[4 * g + 2], d[4 * g + 3]);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        tma_reduce_add_2d(&tmap_dq, stage, (int32_t)(x * 32), row0 + (int32_t)(warp & 3) * 32);
-        bulk_commit_group();
-      }
-    };
 
     for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
       const int32_t key = it.tile * kTile + (int32_t)r;
       const bool key_ok = key < it.L;
       const uint32_t grp_j0 = (uint32_t)(it.tile * kTile) + (warp & 3) * 32 + (lane & ~7u);
       for (int32_t i = 0; i < it.nt; ++i, ++qit) {
-        const uint32_t st = qit & 1;
+        const uint32_t st = qit % kQStages;
         const int32_t qvalid = it.L - i * kTile;          // query rows of this tile inside the sequence
         TR(1);
-        mbar_wait(&sm.qdo_full[st], (qit >> 1) & 1);     // LSE / Delta of this query tile
+        mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);   // LSE / Delta of this query tile
         mbar_wait(&sm.s_full, s_cnt & 1);
         TR(2);
         tc_fence_after();
@@ -353,13 +357,12 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             pd[ch * 16 + e / 2] = pack_bf16(da, db);
           }
         }
-        // grads of the previous tile done: P~^T / dS^T TMEM and dS smem are free, dQ ready
+        // dQ_{i-1} read out of TMEM by the epilogue => grads_{i-1} done: P~^T / dS^T TMEM
+        // and the dS smem tile are free
         TR(4);
-        mbar_wait(&sm.pds_empty, (g_cnt & 1) ^ 1);
+        mbar_wait(&sm.dq_empty, (g_cnt & 1) ^ 1);
         TR(5);
         tc_fence_after();
-        if (has_prev) dq_epilogue(prev_row0);
-        TR(6);
         tmem_st32(t_row + kColP + x * 32, pp);
         tmem_st32(t_row + kColDS + x * 32, pd);
 #pragma unroll
@@ -372,67 +375,101 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         if (lane == 0) mbar_arrive(&sm.pds_full);
         ++g_cnt;
         TR(7);
-        has_prev = true;
-        prev_row0 = (int32_t)((int64_t)it.h * prm.T + it.c0 + i * kTile);
-      }
-      // dK, dV of this key tile
-      TR(8);
-      mbar_wait(&sm.dkv_full, items & 1);
-      TR(9);
-      tc_fence_after();
-      uint32_t kr[32], vr[32];
-      tmem_ld32(t_row + kColDK + x * 32, kr);
-      tmem_ld32(t_row + kColDV + x * 32, vr);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.dkv_free);
-      const float sc = prm.scale;
-      uint32_t pk[16], pv[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        pk[e] = pack_bf16(__uint_as_float(kr[2 * e]) * sc, __uint_as_float(kr[2 * e + 1]) * sc);
-        pv[e] = pack_bf16(__uint_as_float(vr[2 * e]), __uint_as_float(vr[2 * e + 1]));
-      }
-      const int32_t wrow0 = it.tile * kTile + (int32_t)(warp & 3) * 32;   // first key row of this warp
-      if (wrow0 + 32 <= it.L) {
-        // whole warp inside the sequence: stage [32 rows][64 B] x {dK, dV} (64-B swizzle), TMA store
-        stage_free();
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          st_shared_v4(stage_addr + sw64_off(lr, g), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
-          st_shared_v4(stage_addr + 2048 + sw64_off(lr, g), pv[4 * g], pv[4 * g + 1], pv[4 * g + 2], pv[4 * g + 3]);
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          const int32_t row = it.c0 + wrow0;
-          tma_store_2d(&tmap_dkv, stage, (H + it.h) * kD + (int32_t)x * 32, row);
-          tma_store_2d(&tmap_dkv, stage + 2048, (2 * H + it.h) * kD + (int32_t)x * 32, row);
-          bulk_commit_group();
-        }
-      } else if (key_ok) {
-        const int64_t t = (int64_t)it.c0 + key;
-        uint4* dk = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 1) * H + it.h) * kD + x * 32);
-        uint4* dv = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 2) * H + it.h) * kD + x * 32);
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          dk[g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
-          dv[g] = make_uint4(pv[4 * g], pv[4 * g + 1], pv[4 * g + 2], pv[4 * g + 3]);
-        }
       }
     }
-    if (has_prev) {
-      mbar_wait(&sm.pds_empty, (g_cnt & 1) ^ 1);
+  } else if (warp < 12) {
+    // ------------------------------------------------------------ epilogue warpgroup
+    regs_dec<88>();
+    const uint32_t qd = warp & 3;                           // TMEM lane quadrant
+    const uint32_t t_row = tmem + ((qd * 32) << 16);
+    uint8_t* stage = sm.stage[qd];
+    const uint32_t stage_addr = smem_u32(stage);
+    uint32_t e_cnt = 0, items = 0;
+    auto stage_free = [&]() {                               // this warp's previous bulk op read it
+      if (lane == 0) bulk_wait_group_read0();
+      __syncwarp();
+    };
+    WorkItem it;
+    for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 1, it); w += gridDim.x, ++items) {
+      for (int32_t i = 0; i < it.nt; ++i, ++e_cnt) {
+        // dQ_i (query rows 32qd.. of the tile, 64 fp32 columns) -> accumulator (TMA reduce-add)
+        uint32_t d0[32], d1[32];
+        TR(30);
+        mbar_wait(&sm.dq_full, e_cnt & 1);
+        TR(31);
+        tc_fence_after();
+        tmem_ld32(t_row + kColDQ, d0);
+        tmem_ld32(t_row + kColDQ + 32, d1);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.dq_empty);
+        const int32_t row0 = (int32_t)((int64_t)it.h * prm.T + it.c0 + i * kTile) + (int32_t)qd * 32;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const uint32_t* d = half ? d1 : d0;
+          stage_free();
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            st_shared_v4(stage_addr + sw128_off(lane, g), d[4 * g], d[4 * g + 1], d[4 * g + 2], d[4 * g + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(&tmap_dq, stage, half * 32, row0);
+            bulk_commit_group();
+          }
+        }
+        TR(32);
+      }
+      // dK, dV of this key tile (key rows 32qd.., 64 columns each), one after the other
+      TR(33);
+      mbar_wait(&sm.dkv_full, items & 1);
+      TR(34);
       tc_fence_after();
-      dq_epilogue(prev_row0);
+      const int32_t wrow0 = it.tile * kTile + (int32_t)qd * 32;      // first key row of this warp
+      const bool full = wrow0 + 32 <= it.L;                           // whole warp inside the sequence
+      const int64_t t = (int64_t)it.c0 + wrow0 + lane;
+#pragma unroll 1
+      for (int m = 0; m < 2; ++m) {                                   // 0: dK (x scale), 1: dV
+        uint32_t a[32], b[32], pk[32];
+        tmem_ld32(t_row + (m ? kColDV : kColDK), a);
+        tmem_ld32(t_row + (m ? kColDV : kColDK) + 32, b);
+        tmem_ld_wait();
+        if (m == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.dkv_free);
+        }
+        const float sc = m ? 1.f : prm.scale;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          pk[e] = pack_bf16(__uint_as_float(a[2 * e]) * sc, __uint_as_float(a[2 * e + 1]) * sc);
+          pk[16 + e] = pack_bf16(__uint_as_float(b[2 * e]) * sc, __uint_as_float(b[2 * e + 1]) * sc);
+        }
+        if (full) {
+          stage_free();
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            st_shared_v4(stage_addr + sw128_off(lane, g), pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmap_dkv, stage, ((1 + m) * H + it.h) * kD, it.c0 + wrow0);
+            bulk_commit_group();
+          }
+        } else if (wrow0 + (int32_t)lane < it.L) {
+          uint4* dst = reinterpret_cast<uint4*>(prm.dqkv + ((t * 3 + 1 + m) * H + it.h) * kD);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) dst[g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+        }
+      }
     }
     if (lane == 0) bulk_wait_group0();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 13) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -520,7 +557,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
     return st;
   if ((st = make_tmap_f32(&tdq, dq_acc, bwd::kD, (uint64_t)p.T * p.heads, bwd::kD * 4, 32, 32)) != UB_OK) return st;
   if ((st = make_tmap_bf16(&tdkv, dqkv, (uint64_t)3 * p.heads * bwd::kD, (uint64_t)p.T,
-                           (uint64_t)3 * p.heads * bwd::kD * 2, 32, 32, 64)) != UB_OK)
+                           (uint64_t)3 * p.heads * bwd::kD * 2, 64, 32, 128)) != UB_OK)
     return st;
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
   if (p.B > kPlanCap && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 1, v, s)) != UB_OK) return st;

@@ -47,7 +47,7 @@ __device__ __forceinline__ bool decode_item(int32_t w, const FmhaPlanView& v, co
 // sequences by 128-token tile count exactly like fmha_plan_kernel and writes the item
 // prefix, so the persistent kernels need no separate planning launch and decode a work
 // item with a few shared loads.  Larger batches use fmha_plan_kernel + global decode.
-constexpr int kPlanCap = 1024;
+constexpr int kPlanCap = 512;
 struct PlanSmem {
   int32_t prefix[kPlanCap + 1];  // item prefix along the bucketed order
   int32_t seq[kPlanCap];         // sequence id

@@ -125,3 +125,53 @@ def test_nccl_balance_exchange_single_rank(ub):
     assert np.array_equal(os_.cpu().numpy(), exp["samples"])
     assert np.array_equal(ocu.cpu().numpy(), exp["cu"])
     comm.close()
+
+
+@pytest.mark.gpu
+def test_nccl_exchange_two_phase_pipelined(ub):
+    """ub_exchange_begin / ub_exchange_finish with several batches in flight (the bench's
+    pipeline: begin n+2 before finish n+1) give what the oracle's exchange gives per batch."""
+    B, rec, srec = 56, 16, 4
+    comm = ub.Comm(1, 0)
+    side = torch.cuda.Stream()
+    batches = []
+    for k in range(6):
+        lens = synth.gen_lengths(["mlperf_like_v0", "uniform", "bimodal"][k % 3], B, 40 + k)
+        toks = synth.gen_bytes(int(lens.sum()) * rec, 140 + k).reshape(-1, rec)
+        smps = synth.gen_bytes(B * srec, 240 + k).reshape(B, srec)
+        batches.append((lens, toks, smps, torch.from_numpy(lens).cuda(), torch.from_numpy(toks).cuda(),
+                        torch.from_numpy(smps).cuda()))
+    cap = max(int(b[0].sum()) for b in batches)
+    outs = [(torch.empty((cap, rec), dtype=torch.uint8, device="cuda"), torch.empty((B, srec), dtype=torch.uint8,
+             device="cuda"), torch.empty(B + 1, dtype=torch.int32, device="cuda")) for _ in batches]
+    comm.exchange_begin(0, batches[0][3], cap, rec, srec, stream=side)
+    comm.exchange_begin(1, batches[1][3], cap, rec, srec, stream=side)
+    res = []
+    for k in range(len(batches)):
+        ot, os_, ocu = outs[k]
+        res.append(comm.exchange_finish(k % comm.SLOTS, B, batches[k][4], batches[k][5], cap, 512, "paper", ot, os_,
+                                        ocu, stream=side))
+        if k + 2 < len(batches):
+            comm.exchange_begin((k + 2) % comm.SLOTS, batches[k + 2][3], cap, rec, srec, stream=side)
+    side.synchronize()
+    for k, (lens, toks, smps, *_) in enumerate(batches):
+        T, perm = res[k]
+        plan = obal.balance_paper(lens, 1, B)
+        exp = oex.exchange(lens.reshape(1, B), [toks], [smps], plan["perm"], 1, B)[0]
+        assert np.array_equal(perm, plan["perm"]) and T == int(lens.sum())
+        ot, os_, ocu = outs[k]
+        assert np.array_equal(ot[:T].cpu().numpy(), exp["tokens"])
+        assert np.array_equal(os_.cpu().numpy(), exp["samples"])
+        assert np.array_equal(ocu.cpu().numpy(), exp["cu"])
+    # misuse: finish without a begin, begin on a busy slot, slot out of range
+    d = batches[0]
+    with pytest.raises(ub.UbError):
+        comm.exchange_finish(3, B, d[4], d[5], cap, 512, "paper", *outs[0], stream=side)
+    comm.exchange_begin(3, d[3], cap, rec, srec, stream=side)
+    with pytest.raises(ub.UbError):
+        comm.exchange_begin(3, d[3], cap, rec, srec, stream=side)
+    with pytest.raises(ub.UbError):
+        comm.exchange_begin(comm.SLOTS, d[3], cap, rec, srec, stream=side)
+    comm.exchange_finish(3, B, d[4], d[5], cap, 512, "paper", *outs[0], stream=side)
+    side.synchronize()
+    comm.close()
