@@ -135,6 +135,13 @@ __device__ __forceinline__ bool decode_item_smem(int32_t w, const PlanSmem& ps, 
   return true;
 }
 
+// r-th work item of CTA c out of G along the plan, dealt in snake order (round r goes
+// 0..G-1 on even rounds, G-1..0 on odd ones): with items sorted longest first this keeps
+// the per-CTA totals within about one item of each other.
+__device__ __forceinline__ int32_t snake_item(int32_t r, int32_t c, int32_t G) {
+  return r * G + ((r & 1) ? (G - 1 - c) : c);
+}
+
 // Dropout keep bits for 8 consecutive keys j0..j0+7 (j0 % 8 == 0) of packed row t (R5):
 // bit e set <=> key j0+e kept.
 __device__ __forceinline__ uint32_t keep_bits8(uint32_t j0, uint32_t t, uint32_t h, uint32_t off, uint32_t k0,

@@ -17,7 +17,7 @@ f = _lib.lib().ub_debug_bwd_trace; f.restype = C.c_int; f.argtypes = [C.c_void_p
 assert f(buf.ctypes.data_as(C.c_void_p), buf.nbytes) == 0
 ev = (buf >> np.uint64(48)).astype(np.int64); ck = (buf & np.uint64(0xFFFFFFFFFFFF)).astype(np.int64)
 t0 = ck[ck > 0].min()
-names = {1: "c_wait", 2: "S_got", 3: "ld_done", 4: "cmp_done", 5: "pds_empty_ok", 6: "dq_epi_done", 7: "pds_full", 8: "dkv_wait", 9: "dkv_ok",
+names = {11: "S_issued", 19: "grads_issued", 24: "P_lse_st", 1: "c_wait", 2: "S_got", 3: "ld_done", 4: "cmp_done", 5: "pds_empty_ok", 6: "dq_epi_done", 7: "pds_full", 8: "dkv_wait", 9: "dkv_ok",
          10: "S_issue", 12: "grads_issue", 16: "item", 17: "kv_ok", 18: "qdo_ok", 20: "P_item", 21: "P_kv_ok", 22: "P_q", 23: "P_q_ok",
          30: "E_dq_wait", 31: "E_dq_ok", 32: "E_dq_out", 33: "E_dkv_wait", 34: "E_dkv_ok"}
 for w in (0, 4, 8, 12, 13, 14):

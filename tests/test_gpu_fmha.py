@@ -143,8 +143,8 @@ def test_invalid_arguments(ub):
 
 def test_bwd_repeatable_across_changing_batches(ub):
     """Back-to-back backward calls on batches of different T (shared cached workspace)
-    give the same result for the same inputs: dK / dV bit-identical, dQ (fp32 reduce-add,
-    order-nondeterministic, R16) within bf16 rounding."""
+    give bit-identical dQ, dK, dV for the same inputs: every reduction has a fixed order
+    (dQ partials are added pass by pass by one CTA, R16), and no state leaks between calls."""
     outs = []
     for L in ([300, 45, 512, 129], [512, 512, 3], [300, 45, 512, 129]):
         lengths, off, qkv, dout = make_batch(L, 4, 64, seed=77)
@@ -154,8 +154,7 @@ def test_bwd_repeatable_across_changing_batches(ub):
         d = ub.varlen_fmha_bwd(qd, o, lse, gd, cu, 512)
         torch.cuda.synchronize()
         outs.append(d.cpu())
-    assert torch.equal(outs[0][:, 1:], outs[2][:, 1:])
-    assert float((outs[0][:, 0].float() - outs[2][:, 0].float()).abs().max()) < 1e-2
+    assert torch.equal(outs[0], outs[2])
 
 
 def test_bf16_more_sequences_than_smem_plan(ub):
