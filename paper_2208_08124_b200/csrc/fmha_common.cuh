@@ -161,11 +161,11 @@ __device__ __forceinline__ uint32_t keep_bits8(uint32_t j0, uint32_t t, uint32_t
 // `pitch_bytes`, box {64 cols, 128 rows}, 128-B swizzle (matches sdesc_sw128).
 ub_status make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
                          uint32_t box_cols = 64, uint32_t box_rows = 128, int swizzle_bytes = 128);
-// Host: 2-D fp32 tensor map (row-major [rows, cols]), box {box_cols, box_rows}, 128-B swizzle
-// (box_cols * 4 must be 128).
+// Host: 2-D fp32 tensor map (row-major [rows, cols]), box {box_cols, box_rows}, swizzle of
+// box_cols * 4 bytes (128 or 64).
 // Host: 1-D fp32 tensor map over n elements, box of `box` elements (no swizzle).
 ub_status make_tmap_f32_1d(CUtensorMap* map, const void* base, uint64_t n, uint32_t box);
 ub_status make_tmap_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch_bytes,
-                        uint32_t box_cols, uint32_t box_rows);
+                        uint32_t box_cols, uint32_t box_rows, int swizzle_bytes = 128);
 
 }  // namespace ub
