@@ -57,6 +57,99 @@ __global__ void __launch_bounds__(256) unpad_pad_kernel(const Vec* __restrict__ 
   }
 }
 
+// Contiguous-span form for 16-B-aligned rows.  Within sequence b the packed and padded
+// layouts differ by a constant shift: packed vector q <-> padded vector q + delta_b with
+// delta_b = (b*S - cu[b]) * V (V = 16-B vectors per row).  So unpad / pad are B contiguous
+// copies, and pad's zero fill is B contiguous runs whose prefix offsets are the same delta_b.
+// Each CTA takes a fixed span of the packed (or zero) vector space, finds its first
+// sequence by one binary search, and streams 16-B vectors with several loads in flight.
+constexpr int kSpanThreads = 256;
+constexpr int kSpanUnroll = 4;
+constexpr int64_t kSpanVecs = (int64_t)kSpanThreads * kSpanUnroll * 4;   // 64 KB per CTA
+
+__device__ __forceinline__ int32_t seq_of(const int32_t* __restrict__ cu, int32_t B, int64_t key, int64_t V, int32_t S,
+                                          bool zero_space) {
+  // largest b with start_b <= key; start_b = cu[b]*V (packed space) or (b*S - cu[b])*V (zero space)
+  int32_t lo = 0, hi = B - 1;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi + 1) >> 1;
+    const int64_t st = zero_space ? ((int64_t)mid * S - __ldg(cu + mid)) * V : (int64_t)__ldg(cu + mid) * V;
+    if (st <= key) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <bool kPad>
+__global__ void __launch_bounds__(kSpanThreads) span_copy_kernel(const int4* __restrict__ src, int4* __restrict__ dst,
+                                                                 const int32_t* __restrict__ cu, const int4* __restrict__ pad_row,
+                                                                 int32_t B, int32_t S, int64_t V, int64_t n_copy,
+                                                                 int64_t n_zero, int32_t copy_ctas) {
+  const bool zero = kPad && (int32_t)blockIdx.x >= copy_ctas;
+  const int64_t n = zero ? n_zero : n_copy;
+  const int64_t beg = (int64_t)(zero ? blockIdx.x - copy_ctas : blockIdx.x) * kSpanVecs;
+  const int64_t end = min(beg + kSpanVecs, n);
+  if (beg >= end) return;
+  __shared__ int32_t s_b;
+  if (threadIdx.x == 0) s_b = seq_of(cu, B, beg, V, S, zero);
+  __syncthreads();
+  int32_t b = s_b;
+  int64_t q = beg;
+  while (q < end) {
+    // skip empty runs (zero-length sequence, or a full sequence in the zero space)
+    int64_t seg_end, shift;
+    const int64_t c0 = __ldg(cu + b), c1 = __ldg(cu + b + 1);
+    if (!zero) {
+      seg_end = min(end, c1 * V);
+      shift = ((int64_t)b * S - c0) * V;                      // padded = packed + shift
+    } else {
+      seg_end = min(end, ((int64_t)(b + 1) * S - c1) * V);
+      shift = ((int64_t)b * S + (c1 - c0)) * V - ((int64_t)b * S - c0) * V;   // padded = zero index + shift
+    }
+    for (int64_t i0 = q + threadIdx.x; i0 < seg_end; i0 += (int64_t)kSpanThreads * kSpanUnroll) {
+      int4 v[kSpanUnroll];
+#pragma unroll
+      for (int u = 0; u < kSpanUnroll; ++u) {
+        const int64_t i = i0 + (int64_t)u * kSpanThreads;
+        if (i < seg_end) {
+          if (zero) v[u] = pad_row ? __ldg(pad_row + (i + shift) % V) : make_int4(0, 0, 0, 0);
+          else v[u] = kPad ? __ldcs(src + i) : __ldcs(src + i + shift);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kSpanUnroll; ++u) {
+        const int64_t i = i0 + (int64_t)u * kSpanThreads;
+        if (i < seg_end) {
+          if (zero || kPad) __stcs(dst + i + shift, v[u]);
+          else __stcs(dst + i, v[u]);
+        }
+      }
+    }
+    q = seg_end;
+    ++b;
+  }
+}
+
+static ub_status launch_span(bool pad, const void* src, void* dst, const int32_t* d_cu, const void* pad_row, int32_t B,
+                             int32_t S, int64_t T, int64_t row_bytes, cudaStream_t s) {
+  const int64_t V = row_bytes / 16;
+  const int64_t n_copy = T * V, n_zero = pad ? ((int64_t)B * S - T) * V : 0;
+  const int64_t cc = (n_copy + kSpanVecs - 1) / kSpanVecs, zc = (n_zero + kSpanVecs - 1) / kSpanVecs;
+  UB_REQUIRE(cc + zc < (1ll << 31), UB_ERR_UNSUPPORTED, "tensor too large for one launch");
+  if (cc + zc == 0) return UB_OK;
+  const int pk = pad ? kProfPad : kProfUnpad;
+  prof_record(pk, 0, s);
+  if (pad)
+    span_copy_kernel<true><<<(unsigned)(cc + zc), kSpanThreads, 0, s>>>(
+        static_cast<const int4*>(src), static_cast<int4*>(dst), d_cu, static_cast<const int4*>(pad_row), B, S, V, n_copy,
+        n_zero, (int32_t)cc);
+  else
+    span_copy_kernel<false><<<(unsigned)cc, kSpanThreads, 0, s>>>(static_cast<const int4*>(src), static_cast<int4*>(dst),
+                                                                   d_cu, nullptr, B, S, V, n_copy, 0, (int32_t)cc);
+  UB_CHECK_LAUNCH();
+  prof_record(pk, 1, s);
+  return UB_OK;
+}
+
 template <typename Vec>
 static ub_status launch_unpad_pad(bool pad, const void* src, void* dst, const int32_t* d_cu, const void* pad_row,
                                   int32_t B, int32_t S, int64_t row_bytes, cudaStream_t s) {
@@ -92,8 +185,7 @@ static ub_status unpad_pad_dispatch(bool pad, const void* src, void* dst, const 
   UB_REQUIRE(T >= 0 && T <= (int64_t)B * S, UB_ERR_CAPACITY, "T=%lld exceeds B*S", (long long)T);
   const uintptr_t al = (uintptr_t)src | (uintptr_t)dst | (uintptr_t)(pad_row ? pad_row : dst);
   cudaStream_t s = as_stream(stream);
-  if (row_bytes % 16 == 0 && (al & 15) == 0)
-    return launch_unpad_pad<int4>(pad, src, dst, d_cu, pad_row, B, S, row_bytes, s);
+  if (row_bytes % 16 == 0 && (al & 15) == 0) return launch_span(pad, src, dst, d_cu, pad_row, B, S, T, row_bytes, s);
   if (row_bytes % 4 == 0 && (al & 3) == 0)
     return launch_unpad_pad<uint32_t>(pad, src, dst, d_cu, pad_row, B, S, row_bytes, s);
   return launch_unpad_pad<uint8_t>(pad, src, dst, d_cu, pad_row, B, S, row_bytes, s);
