@@ -58,6 +58,14 @@ constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
 constexpr uint32_t kPBytes = kTile * kTile * 2;   // 32 KB
 constexpr int kThreads = 512;
 constexpr uint32_t kQStages = 3;                  // Q / dO / LSE / Delta pipeline depth
+#ifndef UB_BWD_DQ_DIRECT
+#define UB_BWD_DQ_DIRECT 0
+#endif
+// UB_BWD_DQ_DIRECT = 1: the dQ partials of passes before the last go straight from registers
+// to the fp32 scratch (st.global / red.global.add.v4, each lane its own 256-B row) instead of
+// smem staging + TMA store / reduce.  Measured slower (139 vs 113 us on config 2: the L2
+// atomics of 4-KB-per-warp partials are far less efficient than bulk reduces); kept for A/B.
+constexpr bool kDqDirect = UB_BWD_DQ_DIRECT != 0;
 constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDQ = 320, kColDV = 384, kColDK = 448;
 
 struct Smem {
@@ -424,7 +432,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           // this pass's op on tile i follows the previous pass's one (async TMA ops of this
           // warp complete in any order: wait for that group); the last pass re-reads the
           // partial, which is warmed into L1 before dQ is even ready
-          if (!first && full) {
+          if (!first && full && !kDqDirect) {
             if (lane == 0) {
               bulk_wait_group_n((int)(ng - gq[i]));
               if (last) fence_proxy_async_global();
@@ -524,7 +532,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             // pass 0 stores the fp32 partial, middle passes add to it
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
-              if (full) {
+              if (full && !kDqDirect) {
                 stage_free();
 #pragma unroll
                 for (int g = 0; g < 8; ++g)
