@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--dist", default="mlperf_like_v0", choices=list(synth.DISTRIBUTIONS))
     ap.add_argument("--p-dropout", type=float, default=0.0)
-    ap.add_argument("--balance", default="paper", choices=["paper", "snake"])
+    ap.add_argument("--balance", default="paper", choices=["paper", "snake", "lpt"])
     ap.add_argument("--skew", default="iid", choices=["iid", "sorted-block"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -524,13 +524,13 @@ def planned_imbalance(args, steps=20):
     from paper_2208_08124_b200 import api
     out = {}
     for W in (2, 4, 8):
-        rec = {"before": [], "paper": [], "snake": []}
+        rec = {"before": [], "paper": [], "snake": [], "lpt": []}
         for skew in ("iid", "sorted-block"):
             for k in range(steps):
                 a = synth.skewed_rank_lengths(W, B, 1000 + k, skew, args.dist)
                 tok = a.sum(axis=1).astype(np.float64)
                 rec["before"].append(tok.max() / tok.mean() - 1)
-                for mode in ("paper", "snake"):
+                for mode in ("paper", "snake", "lpt"):
                     rt = api.balance_plan(a.reshape(-1), W, B, S, mode)["rank_tokens"].astype(np.float64)
                     rec[mode].append(rt.max() / rt.mean() - 1)
         out[f"w{W}"] = {k: {"mean": round(float(np.mean(v)), 5), "max": round(float(np.max(v)), 5)}

@@ -149,6 +149,11 @@ ub_status ub_varlen_fmha_bwd(const ub_fmha_params* prm, const void* qkv, const v
  *   UB_BAL_SNAKE: same sort, round r dealt to ranks 0..W-1 (r even) or W-1..0 (r odd).
  *   UB_BAL_EXACT_SMALL: exhaustive min-max search over equal-cardinality partitions,
  *     W*B <= 12 else UB_ERR_UNSUPPORTED; ties -> lexicographically smallest perm (R15).
+ *   UB_BAL_LPT: cardinality-constrained longest-processing-time greedy on tokens with
+ *     (max, min) swap refinement, never worse than UB_BAL_PAPER (it falls back to the
+ *     paper's plan when that has a strictly smaller maximum); samples on a rank listed by
+ *     (length asc, id asc).  A beyond-the-paper variant of P:359 (
+ *     steps in DESIGN.md and oracle/balance.py balance_lpt).
  * Outputs (host, caller-allocated):
  *   h_perm [W*B]         perm[r*B + k] = global id of the k-th sample placed on rank r
  *   h_rank_tokens [W]    tokens per rank after the exchange (may be NULL)
@@ -156,11 +161,19 @@ ub_status ub_varlen_fmha_bwd(const ub_fmha_params* prm, const void* qkv, const v
  *   h_send_tokens [W*W]  tokens moving src -> dst (may be NULL)
  * Errors: W < 1, B < 1, a length < 1 -> INVALID_ARG; length > max_seqlen -> CAPACITY.
  */
-typedef enum { UB_BAL_PAPER = 0, UB_BAL_SNAKE = 1, UB_BAL_EXACT_SMALL = 2 } ub_bal_mode;
+typedef enum { UB_BAL_PAPER = 0, UB_BAL_SNAKE = 1, UB_BAL_EXACT_SMALL = 2, UB_BAL_LPT = 3 } ub_bal_mode;
 
 ub_status ub_balance_plan(const int32_t* h_all_lengths, int32_t W, int32_t B, int32_t max_seqlen,
                           int32_t mode, int32_t* h_perm, int64_t* h_rank_tokens,
                           int32_t* h_send_samples, int64_t* h_send_tokens);
+
+/* Cost-aware balancing (NEXT-2): UB_BAL_LPT's steps on the integer per-sample cost
+ * alpha*L + beta*L^2 -- the linear layers grow with L, attention with L^2 (Eq. 1).
+ * For BERT-large one layer's fwd flops per sample are ~ 4096*L*(2048 + L), i.e.
+ * alpha = 2048, beta = 1.  h_rank_cost [W] (may be NULL) = summed cost per rank.
+ * Errors: as ub_balance_plan; alpha < 0, beta < 0, both 0 or above 2^30 -> INVALID_ARG. */
+ub_status ub_balance_plan_weighted(const int32_t* h_all_lengths, int32_t W, int32_t B, int32_t max_seqlen,
+                                   int64_t alpha, int64_t beta, int32_t* h_perm, int64_t* h_rank_cost);
 
 /* ------------------------------------------------------------------------------------
  * Exchange data movement (P:355-359 steps 1 and 3, without the padded all-gather: only

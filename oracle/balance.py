@@ -12,6 +12,8 @@ identical on every worker:
 Also here (reading R15): the snake (boustrophedon) deal, and a brute-force search
 for the min-max-tokens partition with equal cardinality B, by two independent
 enumerators, with the canonical tie-break "lexicographically smallest perm vector".
+Beyond the paper (reading R20, NEXT-2): cardinality-constrained LPT with swap refinement
+on an integer cost alpha*L + beta*L^2, floored by the paper's plan.
 
 Outputs use the library's layout: perm[r*B + k] = global id of the k-th sample on
 rank r; rank_tokens[r]; send_samples[src*W + dst]; send_tokens[src*W + dst].
@@ -20,7 +22,9 @@ Pins (tests/test_oracle_balance.py): SPEC worked examples (S:316 tie order, S:32
 positions 0,2,4, S:336 [[512,512],[64,64]] -> 576/576), permutation + cardinality,
 spread <= Lmax - Lmin, brute force agreement of the two enumerators, the
 counterexample [1,2,3,4] (paper 4/6 vs optimum 5/5), W=1 and B=1 special cases.
-Parity pinned.
+LPT: never above the paper's maximum (by construction, checked), equal to the brute-force
+optimum where the greedy provably is (B = 1: one sample per rank; all lengths equal), a
+hand-worked instance, and max <= OPT + Lmax on random tiny inputs.  Parity pinned.
 """
 from __future__ import annotations
 
@@ -82,6 +86,66 @@ def balance_snake(all_lengths, W, B):
             dst = s if r % 2 == 0 else W - 1 - s
             groups[dst].append(order[r * W + s])
     return plan_from_groups(a, W, B, groups)
+
+
+def balance_lpt(all_lengths, W, B, alpha=1, beta=0):
+    """Beyond the paper (reading R20): cardinality-constrained
+    LPT with (max, min) swap refinement on the integer cost c = alpha*L + beta*L^2, floored by
+    the paper's interleave.  Written as the four steps of DESIGN.md R20, in order:
+      1. ids by (cost desc, id asc); each to the open rank (< B samples) with the least
+         load, lowest rank on ties;
+      2. up to 4*W*B times: M = most loaded rank, m = least loaded (lowest index on ties);
+         over x in M, y in m with d = c[x] - c[y] > 0 take the pair minimising
+         max(load[M] - d, load[m] + d), ties by (x, y) ascending; stop unless it beats
+         load[M]; swap;
+      3. if the paper's plan has a strictly smaller maximum cost, return the paper's plan;
+      4. each rank lists its ids by (length asc, id asc).
+    Returns the plan dict of plan_from_groups plus "rank_cost"."""
+    a = _check(all_lengths, W, B)
+    n = W * B
+    c = [alpha * x + beta * x * x for x in a]
+    order = sorted(range(n), key=lambda g: (-c[g], g))
+    groups = [[] for _ in range(W)]
+    load = [0] * W
+    for g in order:
+        open_ranks = [r for r in range(W) if len(groups[r]) < B]
+        r = min(open_ranks, key=lambda q: (load[q], q))
+        groups[r].append(g)
+        load[r] += c[g]
+    for _ in range(4 * n):
+        if W == 1:
+            break
+        M = max(range(W), key=lambda q: (load[q], -q))
+        m = min(range(W), key=lambda q: (load[q], q))
+        if M == m:
+            break
+        best = None
+        for x in groups[M]:
+            for y in groups[m]:
+                d = c[x] - c[y]
+                if d <= 0:
+                    continue
+                key = (max(load[M] - d, load[m] + d), x, y)
+                if best is None or key < best:
+                    best = key
+        if best is None or best[0] >= load[M]:
+            break
+        _, x, y = best
+        d = c[x] - c[y]
+        groups[M][groups[M].index(x)] = y
+        groups[m][groups[m].index(y)] = x
+        load[M] -= d
+        load[m] += d
+    paper = balance_paper(a, W, B)
+    paper_groups = [list(paper["perm"][r * B:(r + 1) * B]) for r in range(W)]
+    paper_max = max(sum(c[g] for g in grp) for grp in paper_groups)
+    if paper_max < max(load):
+        groups = paper_groups
+    else:
+        groups = [sorted(grp, key=lambda g: (a[g], g)) for grp in groups]
+    out = plan_from_groups(a, W, B, groups)
+    out["rank_cost"] = np.array([sum(c[g] for g in grp) for grp in groups], dtype=np.int64)
+    return out
 
 
 def _canon_group(a, grp):

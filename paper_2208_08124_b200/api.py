@@ -12,9 +12,9 @@ import math
 import numpy as np
 import torch
 
-from ._lib import (UB_BAL_EXACT_SMALL, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BF16, UB_FP32, FmhaParams, check, lib)
+from ._lib import (UB_BAL_EXACT_SMALL, UB_BAL_LPT, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BF16, UB_FP32, FmhaParams, check, lib)
 
-BAL_MODES = {"paper": UB_BAL_PAPER, "snake": UB_BAL_SNAKE, "exact_small": UB_BAL_EXACT_SMALL}
+BAL_MODES = {"paper": UB_BAL_PAPER, "snake": UB_BAL_SNAKE, "exact_small": UB_BAL_EXACT_SMALL, "lpt": UB_BAL_LPT}
 
 
 def _ptr(t):
@@ -149,6 +149,16 @@ def balance_plan(all_lengths, W: int, B: int, max_seqlen: int, mode: str = "pape
     check(lib().ub_balance_plan(_np_ptr(a), W, B, int(max_seqlen), BAL_MODES[mode], _np_ptr(perm), _np_ptr(rt),
                                 _np_ptr(ss), _np_ptr(st)))
     return {"perm": perm, "rank_tokens": rt, "send_samples": ss, "send_tokens": st}
+
+
+def balance_plan_weighted(all_lengths, W: int, B: int, max_seqlen: int, alpha: int, beta: int) -> dict:
+    """Cost-aware planner (NEXT-2): LPT + swaps on alpha*L + beta*L^2; perm, rank_cost."""
+    a = np.ascontiguousarray(np.asarray(all_lengths, dtype=np.int32).reshape(-1))
+    perm = np.zeros(W * B, dtype=np.int32)
+    rc = np.zeros(W, dtype=np.int64)
+    check(lib().ub_balance_plan_weighted(_np_ptr(a), W, B, int(max_seqlen), int(alpha), int(beta), _np_ptr(perm),
+                                         _np_ptr(rc)))
+    return {"perm": perm, "rank_cost": rc}
 
 
 def exchange_tables(all_lengths, perm, W: int, B: int, rank: int, unpack: bool):

@@ -73,6 +73,75 @@ struct ExactSearch {  // exhaustive min-max partition search for W*B <= 12 (R15 
   }
 };
 
+// Cardinality-constrained LPT with (max, min) swap refinement on an integer per-sample cost
+// (NEXT-2 of SURVEY §8(f)).  Steps, as oracle/balance.py:
+//   1. ids by (cost desc, id asc); each goes to the open rank (fewer than B samples) with the
+//      least load, lowest rank on ties;
+//   2. repeat (at most 4*W*B times): M = most loaded rank, m = least loaded (lowest index on
+//      ties); among pairs x in M, y in m with d = c[x] - c[y] > 0 take the one minimising
+//      max(load[M] - d, load[m] + d), ties by (x, y) ascending; stop unless that is < load[M];
+//   3. if the paper's interleave (same cost) has a strictly smaller maximum, use it instead;
+//   4. each rank lists its samples by (length asc, id asc), the paper's order (R12).
+void plan_lpt(const int32_t* a, const std::vector<int64_t>& c, int32_t W, int32_t B, int32_t* perm) {
+  const int32_t n = W * B;
+  std::vector<int32_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&c](int32_t x, int32_t y) { return c[x] > c[y]; });
+  std::vector<std::vector<int32_t>> grp(W);
+  std::vector<int64_t> load(W, 0);
+  for (int32_t g : order) {
+    int32_t best = -1;
+    for (int32_t r = 0; r < W; ++r)
+      if ((int32_t)grp[r].size() < B && (best < 0 || load[r] < load[best])) best = r;
+    grp[best].push_back(g);
+    load[best] += c[g];
+  }
+  for (int32_t iter = 0; iter < 4 * n && W > 1; ++iter) {
+    int32_t M = 0, m = 0;
+    for (int32_t r = 1; r < W; ++r) {
+      if (load[r] > load[M]) M = r;
+      if (load[r] < load[m]) m = r;
+    }
+    if (M == m) break;
+    int64_t best_val = load[M];
+    int32_t bx = -1, by = -1, bi = -1, bj = -1;
+    for (int32_t i = 0; i < B; ++i)
+      for (int32_t j = 0; j < B; ++j) {
+        const int32_t x = grp[M][i], y = grp[m][j];
+        const int64_t d = c[x] - c[y];
+        if (d <= 0) continue;
+        const int64_t v = std::max(load[M] - d, load[m] + d);
+        if (v < best_val || (v == best_val && bx >= 0 && (x < bx || (x == bx && y < by)))) {
+          best_val = v; bx = x; by = y; bi = i; bj = j;
+        }
+      }
+    if (bx < 0) break;
+    const int64_t d = c[bx] - c[by];
+    grp[M][bi] = by;
+    grp[m][bj] = bx;
+    load[M] -= d;
+    load[m] += d;
+  }
+  // the paper's interleave as a floor
+  const auto ids = sorted_ids(a, n);
+  int64_t paper_max = 0, lpt_max = 0;
+  for (int32_t r = 0; r < W; ++r) {
+    int64_t t = 0;
+    for (int32_t k = 0; k < B; ++k) t += c[ids[r + k * W]];
+    paper_max = std::max(paper_max, t);
+    lpt_max = std::max(lpt_max, load[r]);
+  }
+  if (paper_max < lpt_max) {
+    for (int32_t i = 0; i < W; ++i)
+      for (int32_t k = 0; k < B; ++k) perm[i * B + k] = ids[i + k * W];
+    return;
+  }
+  for (int32_t r = 0; r < W; ++r) {
+    std::sort(grp[r].begin(), grp[r].end(), [a](int32_t x, int32_t y) { return a[x] != a[y] ? a[x] < a[y] : x < y; });
+    for (int32_t k = 0; k < B; ++k) perm[r * B + k] = grp[r][k];
+  }
+}
+
 }  // namespace
 }  // namespace ub
 
@@ -101,6 +170,9 @@ extern "C" ub_status ub_balance_plan(const int32_t* a, int32_t W, int32_t B, int
         const int32_t dst = (r % 2 == 0) ? s : W - 1 - s;
         perm[dst * B + r] = ids[r * W + s];
       }
+  } else if (mode == UB_BAL_LPT) {
+    std::vector<int64_t> c(a, a + n);
+    plan_lpt(a, c, W, B, perm);
   } else if (mode == UB_BAL_EXACT_SMALL) {
     UB_REQUIRE(n <= 12, UB_ERR_UNSUPPORTED, "UB_BAL_EXACT_SMALL needs W*B <= 12 (got %d)", n);
     ExactSearch es{a, W, B, n};
@@ -124,6 +196,31 @@ extern "C" ub_status ub_balance_plan(const int32_t* a, int32_t W, int32_t B, int
       const int32_t g = perm[dst * B + k], src = g / B;
       if (send_samples) send_samples[src * W + dst] += 1;
       if (send_tokens) send_tokens[src * W + dst] += a[g];
+    }
+  return UB_OK;
+}
+
+extern "C" ub_status ub_balance_plan_weighted(const int32_t* a, int32_t W, int32_t B, int32_t max_seqlen,
+                                              int64_t alpha, int64_t beta, int32_t* perm, int64_t* rank_cost) {
+  clear_error();
+  UB_REQUIRE(a && perm, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(W >= 1 && B >= 1, UB_ERR_INVALID_ARG, "W=%d B=%d", W, B);
+  UB_REQUIRE((int64_t)W * B <= (1 << 30), UB_ERR_SHAPE, "W*B too large");
+  UB_REQUIRE(alpha >= 0 && beta >= 0 && (alpha > 0 || beta > 0), UB_ERR_INVALID_ARG, "need alpha, beta >= 0, not both 0");
+  UB_REQUIRE(alpha <= (1ll << 30) && beta <= (1ll << 30), UB_ERR_INVALID_ARG, "weights above 2^30");
+  const int32_t n = W * B;
+  std::vector<int64_t> c(n);
+  for (int32_t g = 0; g < n; ++g) {
+    UB_REQUIRE(a[g] >= 1, UB_ERR_INVALID_ARG, "length[%d] = %d < 1", g, a[g]);
+    UB_REQUIRE(a[g] <= max_seqlen, UB_ERR_CAPACITY, "length[%d] = %d > max_seqlen %d", g, a[g], max_seqlen);
+    c[g] = alpha * a[g] + beta * (int64_t)a[g] * a[g];
+  }
+  plan_lpt(a, c, W, B, perm);
+  if (rank_cost)
+    for (int32_t r = 0; r < W; ++r) {
+      int64_t t = 0;
+      for (int32_t k = 0; k < B; ++k) t += c[perm[r * B + k]];
+      rank_cost[r] = t;
     }
   return UB_OK;
 }

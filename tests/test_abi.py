@@ -98,6 +98,26 @@ def test_balance_plan_exact_small_bit_exact(ub):
     assert e.value.status == 3
 
 
+def test_balance_plan_lpt_bit_exact(ub):
+    """UB_BAL_LPT and ub_balance_plan_weighted vs oracle balance_lpt (R20), bit-exact."""
+    from paper_2208_08124_b200 import api
+    rng = np.random.default_rng(5)
+    for W in (1, 2, 3, 8):
+        for B in (1, 2, 7, 56):
+            for _ in range(3):
+                a = rng.integers(1, 513, size=W * B).astype(np.int32)
+                got = api.balance_plan(a, W, B, 512, "lpt")
+                exp = obal.balance_lpt(a, W, B)
+                for k in ("perm", "rank_tokens", "send_samples", "send_tokens"):
+                    assert np.array_equal(np.asarray(got[k], np.int64), np.asarray(exp[k], np.int64)), (W, B, k)
+                gw = api.balance_plan_weighted(a, W, B, 512, 2048, 1)
+                ew = obal.balance_lpt(a, W, B, alpha=2048, beta=1)
+                assert np.array_equal(gw["perm"].astype(np.int64), ew["perm"]) and np.array_equal(gw["rank_cost"], ew["rank_cost"])
+    from paper_2208_08124_b200 import UbError
+    with pytest.raises(UbError):
+        api.balance_plan_weighted([1, 2], 2, 1, 512, 0, 0)
+
+
 def test_exchange_tables_reproduce_oracle_exchange(ub):
     """Apply the library's pack/unpack tables with plain numpy copies (the device kernel
     only follows the table) and compare the bytes every rank ends with to the oracle."""

@@ -130,3 +130,66 @@ def test_exchange_simulation():
             a0, a1 = out[d]["cu"][k], out[d]["cu"][k + 1]
             assert np.array_equal(out[d]["tokens"][a0:a1], toks[s][offs[s][kk]:offs[s][kk + 1]])
             assert np.array_equal(out[d]["samples"][k], smps[s][kk])
+
+
+# ---------------------------------------------------------------- LPT (reading R20, NEXT-2)
+def test_lpt_hand_worked_instances():
+    """Worked by hand from the four steps of R20."""
+    # [1,2,3,4], W=2: greedy 4->r0, 3->r1, 2->r1, 1->r0 => {1,4} {2,3}: 5/5 (the optimum;
+    # the paper's interleave gives 4/6)
+    plan = balance.balance_lpt([1, 2, 3, 4], 2, 2)
+    assert list(plan["perm"]) == [0, 3, 1, 2] and list(plan["rank_tokens"]) == [5, 5]
+    # [5,1,1,1,4,2], W=2, B=3: 5->r0, 4->r1, 2->r1, 1->r0, 1->r0 (tie -> r0), 1->r1 (r0 full)
+    plan = balance.balance_lpt([5, 1, 1, 1, 4, 2], 2, 3)
+    assert list(plan["perm"]) == [1, 2, 0, 3, 5, 4] and list(plan["rank_tokens"]) == [7, 7]
+
+
+def test_lpt_invariants_floor_and_optimality_cases():
+    rng = np.random.default_rng(20)
+    for _ in range(300):
+        W = int(rng.integers(1, 5)); B = int(rng.integers(1, 4))
+        a = rng.integers(1, 40, size=W * B).tolist()
+        plan = balance.balance_lpt(a, W, B)
+        perm = plan["perm"]
+        assert sorted(perm.tolist()) == list(range(W * B))                        # a permutation
+        assert plan["rank_tokens"].max() <= balance.balance_paper(a, W, B)["rank_tokens"].max()   # floor
+        for r in range(W):                                                        # order within a rank
+            grp = perm[r * B:(r + 1) * B]
+            assert [(a[g], g) for g in grp] == sorted((a[g], g) for g in grp)
+        if W * B <= 9:
+            opt = balance.balance_opt(a, W, B)["opt_max_tokens"]
+            assert plan["rank_tokens"].max() <= opt + max(a)                      # LPT bound
+            if B == 1:
+                assert plan["rank_tokens"].max() == opt                           # one sample per rank
+    # all lengths equal: perfect balance
+    plan = balance.balance_lpt([7] * 12, 4, 3)
+    assert set(plan["rank_tokens"].tolist()) == {21}
+    # W = 1: everything on rank 0, ascending
+    plan = balance.balance_lpt([3, 1, 2], 1, 3)
+    assert list(plan["perm"]) == [1, 2, 0]
+
+
+def test_lpt_weighted_cost():
+    """alpha*L + beta*L^2: with beta = 0 it is the token LPT scaled; with a quadratic cost the
+    rank costs are what the plan's groups sum to."""
+    rng = np.random.default_rng(21)
+    for _ in range(50):
+        W, B = 4, 5
+        a = rng.integers(1, 512, size=W * B).tolist()
+        p1 = balance.balance_lpt(a, W, B)
+        p3 = balance.balance_lpt(a, W, B, alpha=3, beta=0)
+        assert np.array_equal(p1["perm"], p3["perm"]) and np.array_equal(3 * p1["rank_tokens"], p3["rank_cost"])
+        q = balance.balance_lpt(a, W, B, alpha=2048, beta=1)
+        c = [2048 * x + x * x for x in a]
+        assert [sum(c[g] for g in q["perm"][r * B:(r + 1) * B]) for r in range(W)] == q["rank_cost"].tolist()
+
+
+def test_lpt_balances_far_better_at_8():
+    """SURVEY Appendix A simulation: mean imbalance 1.6% (paper) vs ~0.01% (LPT) at W=8."""
+    from synth import gen_lengths
+    imb_p, imb_l = [], []
+    for s in range(10):
+        a = gen_lengths("mlperf_like_v0", 8 * 56, 100 + s)
+        imb_p.append(balance.imbalance(balance.balance_paper(a, 8, 56)["rank_tokens"]))
+        imb_l.append(balance.imbalance(balance.balance_lpt(a, 8, 56)["rank_tokens"]))
+    assert np.mean(imb_l) < 0.002 < np.mean(imb_p)
