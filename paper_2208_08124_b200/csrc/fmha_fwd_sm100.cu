@@ -18,8 +18,8 @@
 //               item's first), so the softmax never waits for an item boundary
 //   warps 10-11 idle (the third warpgroup is whole so that setmaxnreg can move registers
 //               from it to the softmax warpgroups: 208 vs 88 per thread)
-// The softmax warpgroups take turns for their exp phases (named-barrier token), and each
-// defers its epilogue (O / l -> bf16 -> TMA store, LSE) into the first key tile of its
+// Optionally (UB_FWD_EXP_TURNS) the softmax warpgroups take turns for their exp phases
+// (named-barrier token; measured neutral, off by default).  Each warpgroup defers its epilogue (O / l -> bf16 -> TMA store, LSE) into the first key tile of its
 // next item, after that tile's P has been handed to the MMA.
 // TMEM (512 columns): per warpgroup x: S at 256x (128 cols fp32), P at 256x+128 (64 cols,
 // bf16 pairs), O at 256x+192 (64 cols fp32).
@@ -60,7 +60,7 @@ constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
 constexpr int kThreads = UB_FWD_SETMAXNREG ? 384 : 320;   // 3 warpgroups (setmaxnreg is per warpgroup)
 constexpr float kRescaleThreshold = 8.0f;         // log2 units
 #ifndef UB_FWD_EXP_TURNS
-#define UB_FWD_EXP_TURNS 1
+#define UB_FWD_EXP_TURNS 0   // measured neutral on config 2 (60.4-61.3 us either way); kept for A/B
 #endif
 constexpr bool kExpTurns = UB_FWD_EXP_TURNS != 0;
 
