@@ -460,6 +460,15 @@ def run_ours(args, world, rank, local):
                "pad": {"us": round(pad_us, 2), "GBps": round(pad_gbs, 1), "frac_hbm": round(pad_gbs / peaks["hbm"], 3)},
                "unpad_records": {"us": round(unpad_us, 2)}}
     fmha_only = mean_T * world / ((fwd_us + bwd_us) * 1e-6)
+    # main-stream timeline from the same events: idle gap before each step's forward (after
+    # the previous pad), forward end -> backward main kernel (= Delta prologue + gap), backward
+    # end -> pad start
+    P = prof_events
+    F, Bk, Pd = kids[0], kids[1], kids[2]
+    timeline = {
+        "gap_before_fwd_us": round(float(np.mean([P[i - 1][Pd][1].elapsed_time(P[i][F][0]) for i in range(1, args.steps)])) * 1e3, 2),
+        "fwd_end_to_bwd_main_us": round(float(np.mean([P[i][F][1].elapsed_time(P[i][Bk][0]) for i in range(args.steps)])) * 1e3, 2),
+        "bwd_end_to_pad_us": round(float(np.mean([P[i][Bk][1].elapsed_time(P[i][Pd][0]) for i in range(args.steps)])) * 1e3, 2)}
 
     e2e = None if args.no_e2e else run_e2e(args, wl, world)
     gather = gather_bench(wl, peaks) if rank == 0 else None
@@ -473,7 +482,7 @@ def run_ours(args, world, rank, local):
                       "step": "unpad records + exchange (side stream) | fmha fwd + bwd + pad (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
-           "gather": gather, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
+           "main_stream_timeline": timeline, "gather": gather, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
            "host_us_per_step": dict(zip(["step_setup", "fwd_call", "bwd_call", "pad_call", "unpad_call", "finish_call",
                                               "begin_call"],
                                         [round(1e6 * float(x), 1) for x in np.median(np.array(marks), axis=0)]),

@@ -149,7 +149,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     if (lane == 0) {
       uint32_t items = 0, kv_it = 0;
       WorkItem it;
-      for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x, ++items) {
+      for (int32_t r = 0; decode_item_smem<kBigB>(snake_item(r, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); ++r, ++items) {
         const uint32_t slot = items & 1;
         TR(20);
         mbar_wait(&sm.q_empty[slot], ((items >> 1) & 1) ^ 1);
@@ -189,8 +189,8 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         ++s_cnt[x];
       };
       WorkItem it, nit;
-      int32_t w = blockIdx.x;
-      bool have = decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it);
+      int32_t r = 0;                                      // this CTA's item round (snake order)
+      bool have = decode_item_smem<kBigB>(snake_item(0, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, it);
       uint32_t items = 0, kv_it = 0;
       if (have) {
         mbar_wait(&sm.q_full[0], 0);
@@ -214,7 +214,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           if (j + 1 < it.nt) {
             nxt_tiles = nx;
           } else {
-            have_next_item = decode_item_smem<kBigB>(w + (int32_t)gridDim.x, sm.plan, prm.plan, prm.cu, prm.B, H, 2, nit);
+            have_next_item = decode_item_smem<kBigB>(snake_item(r + 1, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, nit);
             if (have_next_item) {
               nxt_tiles = nit.ntile;
               nslot = slot ^ 1u;
@@ -249,7 +249,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         umma_commit(&sm.q_empty[slot]);
         kv_it += it.nt;
         ++items;
-        w += gridDim.x;
+        ++r;
         have = have_next_item;
         it = nit;
       }
@@ -319,7 +319,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     // through the key tiles of single-tile items it sits out.
     if (kExpTurns && x == 1) named_bar_arrive(1, 256);
     WorkItem it;
-    for (int32_t w = blockIdx.x; decode_item_smem<kBigB>(w, sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); w += gridDim.x) {
+    for (int32_t ri = 0; decode_item_smem<kBigB>(snake_item(ri, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); ++ri) {
       if (x >= it.ntile) {
         if (kExpTurns)
           for (int32_t j = 0; j < it.nt; ++j) {
