@@ -256,10 +256,12 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         umma_commit(&sm.qdo_empty[p_st]);              // Q_i / dO_i no longer needed
         mbar_wait(&sm.dq_empty, (g_cnt & 1) ^ 1);      // the epilogue has read dQ of the previous pair
         tc_fence_after();
+#ifndef UB_BWD_EXPERIMENT_NO_DQ_MMA
 #pragma unroll
         for (uint32_t k = 0; k < kTile / 16; ++k)        // dQ = dS K, K = key rows, 16 per MMA
           umma_bf16_ss(tmem + kColDQ, sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024),
                        sdesc_sw128(p_kaddr + k * 2048, 8192, 1024), kIdescQ, k > 0);
+#endif
         umma_commit(&sm.dq_full);                      // grads done: P~^T / dS free, dQ_i in TMEM
         TR(19);
         ++g_cnt;
@@ -278,7 +280,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           TR(17);
           for (int32_t i = 0; i < it.nt; ++i, ++qit) {
             const uint32_t st = qit % kQStages;
+#ifndef UB_BWD_EXPERIMENT_NO_QDO_WAIT
             mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);
+#endif
             TR(18);
             mbar_wait(&sm.s_free, (s_cnt & 1) ^ 1);
             TR(10);
@@ -379,7 +383,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           }
           // grads of the previous pair done => P~^T TMEM and the dS smem tile are free
           TR(4);
+#ifndef UB_BWD_EXPERIMENT_NO_GRAD_WAIT
           mbar_wait(&sm.dq_full, (g_cnt & 1) ^ 1);
+#endif
           TR(5);
           tc_fence_after();
           tmem_st32(t_row + kColP + x * 32, pp);
@@ -541,8 +547,13 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
+#if defined(UB_BWD_EXPERIMENT_NO_DQ_OUT)   // timing experiments only (wrong dQ)
+#elif defined(UB_BWD_EXPERIMENT_DQ_STORE_ONLY)
+                  tma_store_2d(&tmap_dq, stage, half * 32, arow0);
+#else
                   if (first) tma_store_2d(&tmap_dq, stage, half * 32, arow0);
                   else tma_reduce_add_2d(&tmap_dq, stage, half * 32, arow0);
+#endif
                   bulk_commit_group();
                   ++ng;
                 }
