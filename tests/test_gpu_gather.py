@@ -68,15 +68,20 @@ def test_unpad_unaligned_and_errors(ub):
     assert e.value.status == 3
 
 
-@pytest.mark.parametrize("W,rec,srec", [(2, 16, 4), (4, 16, 4), (8, 16, 4), (3, 2048, 8), (5, 6, 3)])
-def test_exchange_pack_transport_unpack_virtual_ranks(ub, W, rec, srec):
+@pytest.mark.parametrize("W,rec,srec,mode", [(2, 16, 4, "paper"), (4, 16, 4, "paper"), (8, 16, 4, "paper"),
+                                              (3, 2048, 8, "paper"), (5, 6, 3, "paper"), (8, 16, 4, "lpt"),
+                                              (3, 2048, 8, "lpt")])
+def test_exchange_pack_transport_unpack_virtual_ranks(ub, W, rec, srec, mode):
     """W virtual ranks on one GPU: pack (kernel) -> transport (per-peer slices, as the
-    grouped ncclSend/ncclRecv moves them) -> unpack (kernel); bytes equal the oracle."""
+    grouped ncclSend/ncclRecv moves them) -> unpack (kernel); bytes equal the oracle
+    (paper plan, and the LPT plan of reading R20)."""
     B = 56 if rec <= 16 else 9
     lens = synth.skewed_rank_lengths(W, B, 0, "sorted-block")
     toks = [synth.gen_bytes(int(lens[r].sum()) * rec, 70 + r).reshape(-1, rec) for r in range(W)]
     smps = [synth.gen_bytes(B * srec, 80 + r).reshape(B, srec) for r in range(W)]
-    plan = ub.balance_plan(lens.reshape(-1), W, B, 512, "paper")
+    plan = ub.balance_plan(lens.reshape(-1), W, B, 512, mode)
+    ref = (obal.balance_paper if mode == "paper" else obal.balance_lpt)(lens.reshape(-1), W, B)
+    assert np.array_equal(np.asarray(plan["perm"], np.int64), np.asarray(ref["perm"], np.int64))
     exp = oex.exchange(lens, toks, smps, plan["perm"], W, B)
     send = []
     for r in range(W):
