@@ -389,11 +389,17 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           TR(5);
           tc_fence_after();
           tmem_st32(t_row + kColP + x * 32, pp);
+#ifndef UB_BWD_EXPERIMENT_NO_DS_STS
 #pragma unroll
           for (int g = 0; g < 8; ++g)
             st_shared_v4(ds_addr + sw128_off(r, g), pd[4 * g], pd[4 * g + 1], pd[4 * g + 2], pd[4 * g + 3]);
+#else
+          if (pd[0] == 0x7fc07fc0u && pd[31] == 0x7fc07fc0u) st_shared_v4(ds_addr, pd[1], pd[2], pd[3], pd[4]);
+#endif
           tmem_st_wait();
+#ifndef UB_BWD_EXPERIMENT_NO_DS_FENCE
           fence_proxy_async_smem();
+#endif
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.pds_full);
