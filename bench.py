@@ -523,6 +523,30 @@ def gather_bench(wl, peaks, iters=20):
         out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
                      "bytes": int(nbytes)}
     out["shape"] = f"hidden [{B}, {S}, {H * D}] bf16 <-> [T={T}, {H * D}]"
+    # NEXT-1 piece: Dropout_Add_LayerNorm on the same packed hidden state, p = 0.1
+    E = H * D
+    hs = [tuple(torch.randn((T, E), device=wl.dev).to(torch.bfloat16) for _ in range(3)) for _ in range(3)]
+    g = torch.ones(E, dtype=torch.bfloat16, device=wl.dev)
+    bt = torch.zeros(E, dtype=torch.bfloat16, device=wl.dev)
+    st = [ub.dal_fwd(h[0], h[1], g, bt, 0.1, 1e-12, 5) for h in hs]
+    for name, kid, fn, nbytes in (
+            ("dal_fwd", api.PROF_DAL_FWD, lambda k: ub.dal_fwd(hs[k][0], hs[k][1], g, bt, 0.1, 1e-12, 5), 3 * T * E * 2 + 8 * T),
+            ("dal_bwd", api.PROF_DAL_BWD,
+             lambda k: ub.dal_bwd(hs[k][2], hs[k][0], hs[k][1], g, st[k][1], st[k][2], 0.1, 5), 5 * T * E * 2 + 8 * T)):
+        for k in range(3):
+            fn(k)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        torch.cuda._sleep(2_000_000)
+        for k in range(iters):
+            api.profile_events(kid, *ev[k])
+            fn(k % 3)
+        api.profile_events(kid)
+        torch.cuda.synchronize()
+        us = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
+        gbs = nbytes / (us * 1e-6) / 1e9
+        out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
+                     "bytes": int(nbytes), "p_dropout": 0.1}
     return out
 
 

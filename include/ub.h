@@ -141,6 +141,26 @@ ub_status ub_varlen_fmha_bwd(const ub_fmha_params* prm, const void* qkv, const v
                              void* dqkv, void* ws, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * Dropout_Add_LayerNorm (§IV-C-1 kernel fusion; SURVEY §8(f) NEXT-1 piece): one
+ * forward kernel, two backward kernels, on packed rows (no padding).
+ *   z = res + a * keep / (1 - p),  y = (z - mean) * rstd * gamma + beta,  rstd = 1/sqrt(var + eps)
+ *   keep: Philox4x32-10, key = seed, counter = (col >> 3, row, 0xDA100000, offset),
+ *   16-bit half (col & 1) of word ((col & 7) >> 1) >= floor(p * 65536)   (reading R21)
+ * Layouts (device, caller-allocated, 16-B aligned): a, res, y, dy, da, dres [T, E] bf16;
+ * gamma, beta [E] bf16; mean, rstd [T] fp32 (written by the forward, read by the backward);
+ * dgamma, dbeta [E] fp32.  E a multiple of 8 in [8, 2048] else UB_ERR_UNSUPPORTED;
+ * p in [0, 1), eps > 0 else UB_ERR_INVALID_ARG.  The mask is regenerated, never stored.
+ * Backward workspace: ub_dal_bwd_workspace_bytes(T, E) bytes (per-CTA partial sums; the
+ * reduction order is fixed, so dgamma / dbeta are bitwise deterministic).  Async on stream. */
+ub_status ub_dal_fwd(const void* a, const void* res, const void* gamma, const void* beta, int64_t T, int32_t E,
+                     float p_dropout, float eps, uint64_t seed, uint64_t offset, void* y, float* mean, float* rstd,
+                     void* stream);
+size_t ub_dal_bwd_workspace_bytes(int64_t T, int32_t E);
+ub_status ub_dal_bwd(const void* dy, const void* a, const void* res, const void* gamma, const float* mean,
+                     const float* rstd, int64_t T, int32_t E, float p_dropout, uint64_t seed, uint64_t offset,
+                     void* da, void* dres, float* dgamma, float* dbeta, void* ws, void* stream);
+
+/* ------------------------------------------------------------------------------------
  * Padding-exchange balancer (§IV-B-1).  Pure host function: deterministic,
  * byte-identical on every rank given the same all-gathered lengths.
  *   h_all_lengths [W*B]: rank-major all-gather of the valid lengths, global id g = r*B+k.

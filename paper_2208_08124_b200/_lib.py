@@ -36,6 +36,9 @@ SIGNATURES = {
     "ub_fmha_workspace_bytes": (sz, [C.POINTER(FmhaParams), C.c_int]),
     "ub_varlen_fmha_fwd": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, vp]),
     "ub_varlen_fmha_bwd": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, vp, vp, vp]),
+    "ub_dal_fwd": (i32, [vp, vp, vp, vp, i64, i32, f32, f32, u64, u64, vp, vp, vp, vp]),
+    "ub_dal_bwd_workspace_bytes": (sz, [i64, i32]),
+    "ub_dal_bwd": (i32, [vp, vp, vp, vp, vp, vp, i64, i32, f32, u64, u64, vp, vp, vp, vp, vp, vp]),
     "ub_balance_plan": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp]),
     "ub_balance_plan_weighted": (i32, [vp, i32, i32, i32, i64, i64, vp, vp]),
     "ub_exchange_tables": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),

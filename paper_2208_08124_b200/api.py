@@ -46,12 +46,12 @@ def version() -> str:
     return lib().ub_version().decode()
 
 
-PROF_FWD, PROF_BWD, PROF_PAD, PROF_UNPAD = 0, 1, 2, 3
+PROF_FWD, PROF_BWD, PROF_PAD, PROF_UNPAD, PROF_DAL_FWD, PROF_DAL_BWD = 0, 1, 2, 3, 4, 5
 
 
 def profile_events(kernel_id: int, start=None, stop=None):
     """Record torch.cuda.Event `start`/`stop` around every launch of one internal kernel
-    (0 fwd main, 1 bwd main, 2 pad, 3 unpad); None clears.  Bench/profiling hook."""
+    (0 fwd main, 1 bwd main, 2 pad, 3 unpad, 4 DAL fwd, 5 DAL bwd incl. its reduction); None clears.  Bench/profiling hook."""
     for e in (start, stop):
         if e is not None and not e.cuda_event:
             e.record()            # torch creates the cudaEvent_t lazily on first record
@@ -136,6 +136,34 @@ def varlen_fmha_bwd(qkv, out, lse, dout, cu, max_seqlen: int, scale=None, p_drop
     check(lib().ub_varlen_fmha_bwd(C.byref(prm), _ptr(qkv), _ptr(out), _ptr(lse), _ptr(dout), _ptr(cu),
                                    _ptr(dqkv), _ptr(ws), _stream(stream)))
     return dqkv
+
+
+# ------------------------------------------------------------------ Dropout_Add_LayerNorm
+def dal_fwd(a: torch.Tensor, res: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, p_dropout=0.0, eps=1e-12,
+            seed=0, offset=0, out=None, mean=None, rstd=None, stream=None):
+    """y = LayerNorm(res + dropout(a)) * gamma + beta over packed rows (R21).
+    a, res [T, E] bf16; gamma, beta [E] bf16.  Returns (y [T, E] bf16, mean [T], rstd [T] fp32)."""
+    T, E = a.shape
+    y = out if out is not None else torch.empty_like(a)
+    mean = mean if mean is not None else torch.empty(T, dtype=torch.float32, device=a.device)
+    rstd = rstd if rstd is not None else torch.empty(T, dtype=torch.float32, device=a.device)
+    check(lib().ub_dal_fwd(_ptr(a), _ptr(res), _ptr(gamma), _ptr(beta), int(T), int(E), float(p_dropout), float(eps),
+                           int(seed), int(offset), _ptr(y), _ptr(mean), _ptr(rstd), _stream(stream)))
+    return y, mean, rstd
+
+
+def dal_bwd(dy: torch.Tensor, a: torch.Tensor, res: torch.Tensor, gamma: torch.Tensor, mean: torch.Tensor,
+            rstd: torch.Tensor, p_dropout=0.0, seed=0, offset=0, stream=None):
+    """Backward of dal_fwd: returns (da, dres [T, E] bf16, dgamma, dbeta [E] fp32)."""
+    T, E = a.shape
+    da, dres = torch.empty_like(a), torch.empty_like(a)
+    dgamma = torch.empty(E, dtype=torch.float32, device=a.device)
+    dbeta = torch.empty(E, dtype=torch.float32, device=a.device)
+    ws = _workspace(lib().ub_dal_bwd_workspace_bytes(int(T), int(E)), a.device, "dal_bwd")
+    check(lib().ub_dal_bwd(_ptr(dy), _ptr(a), _ptr(res), _ptr(gamma), _ptr(mean), _ptr(rstd), int(T), int(E),
+                           float(p_dropout), int(seed), int(offset), _ptr(da), _ptr(dres), _ptr(dgamma), _ptr(dbeta),
+                           _ptr(ws), _stream(stream)))
+    return da, dres, dgamma, dbeta
 
 
 # ------------------------------------------------------------------ balancer

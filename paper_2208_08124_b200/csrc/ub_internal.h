@@ -16,7 +16,7 @@ void clear_error();
 ub_status require_sm100();
 
 // Measurement hook (ub_profile_events): events recorded around one internal kernel.
-enum ProfKernel { kProfFwd = 0, kProfBwd = 1, kProfPad = 2, kProfUnpad = 3, kProfCount = 4 };
+enum ProfKernel { kProfFwd = 0, kProfBwd = 1, kProfPad = 2, kProfUnpad = 3, kProfDalFwd = 4, kProfDalBwd = 5, kProfCount = 6 };
 void prof_record(int kernel_id, int which, cudaStream_t s);
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device).
