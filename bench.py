@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--skew", default="iid", choices=["iid", "sorted-block"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-encoder", action="store_true", help="skip the NEXT-1 encoder sub-layer measurement")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--reserve-sms", type=int, default=4)
     return ap.parse_args()
@@ -472,6 +473,7 @@ def run_ours(args, world, rank, local):
 
     e2e = None if args.no_e2e else run_e2e(args, wl, world)
     gather = gather_bench(wl, peaks) if rank == 0 else None
+    encoder = encoder_bench(wl, peaks) if rank == 0 and not args.no_encoder else None
     out = {"metric": "unpadded FMHA fwd+bwd tokens/s (BERT-large)", "value": round(value, 1), "unit": "tokens/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -482,7 +484,7 @@ def run_ours(args, world, rank, local):
                       "step": "unpad records + exchange (side stream) | fmha fwd + bwd + pad (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
-           "main_stream_timeline": timeline, "gather": gather, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
+           "main_stream_timeline": timeline, "gather": gather, "encoder_attn_sublayer": encoder, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
            "host_us_per_step": dict(zip(["step_setup", "fwd_call", "bwd_call", "pad_call", "unpad_call", "finish_call",
                                               "begin_call"],
                                         [round(1e6 * float(x), 1) for x in np.median(np.array(marks), axis=0)]),
@@ -547,6 +549,53 @@ def gather_bench(wl, peaks, iters=20):
         gbs = nbytes / (us * 1e-6) / 1e9
         out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
                      "bytes": int(nbytes), "p_dropout": 0.1}
+    return out
+
+
+def encoder_bench(wl, peaks, iters=10):
+    """NEXT-1 (BASELINE config 4 on one GPU): the unpadded encoder attention sub-layer
+    (QKV Linear -> varlen FMHA -> out Linear -> Dropout_Add_LayerNorm) forward and backward
+    on the config-2 batch, hidden 1024, p_attn = p_hidden = 0.1, random-init weights.
+    Algorithmic flops: GEMMs 8*T*h^2 fwd / 16*T*h^2 bwd, attention 4 / 8 *H*D*sum(L^2)."""
+    ub = wl.ub
+    st = wl.sets[0]
+    T, cu = st["T"], st["cu_local"]
+    L = np.diff(cu.cpu().numpy().astype(np.int64))
+    hid = H * D
+    dev = wl.dev
+    s = 1.0 / math.sqrt(hid)
+    w = {k: (torch.randn(shape, device=dev) * sc).to(torch.bfloat16) for k, shape, sc in
+         (("wq", (3 * hid, hid), s), ("bq", (3 * hid,), 0.1), ("wo", (hid, hid), s), ("bo", (hid,), 0.1),
+          ("g", (hid,), 0.0), ("b", (hid,), 0.1))}
+    w["g"] += 1.0
+    xs = [torch.randn((T, hid), device=dev).to(torch.bfloat16) for _ in range(3)]
+    dys = [torch.randn((T, hid), device=dev).to(torch.bfloat16) for _ in range(3)]
+    saved = [None] * 3
+    fwd = lambda k: ub.encoder_attn_fwd(xs[k], cu, S, w["wq"], w["bq"], w["wo"], w["bo"], w["g"], w["b"], H, 0.1, 0.1,
+                                        1e-12, 0x2208 + k, 0, saved=saved[k])
+    for k in range(3):
+        saved[k] = fwd(k)[1]
+    bwd = lambda k: ub.encoder_attn_bwd(dys[k], xs[k], cu, S, w["wq"], w["wo"], w["g"], saved[k], H, 0.1, 0.1, 1e-12,
+                                        0x2208 + k, 0)
+    out = {}
+    s2 = float((L ** 2).sum())
+    for name, fn, fl in (("fwd", fwd, 8 * T * hid * hid + 4 * H * D * s2),
+                         ("bwd", bwd, 16 * T * hid * hid + 8 * H * D * s2)):
+        for k in range(3):
+            fn(k)
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(iters):
+            fn(k % 3)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / iters * 1e3
+        tf = fl / (us * 1e-6) / 1e12
+        out[name] = {"us": round(us, 1), "tflops": round(tf, 1), "frac_bf16_peak": round(tf / peaks["bf16"], 3)}
+    out["tokens_per_s_fwd_bwd"] = round(T / ((out["fwd"]["us"] + out["bwd"]["us"]) * 1e-6), 1)
+    out["config"] = f"T={T} (config-2 batch), hidden {hid}, heads {H}, p_attn = p_hidden = 0.1, GEMMs via cuBLASLt"
     return out
 
 

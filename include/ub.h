@@ -161,6 +161,54 @@ ub_status ub_dal_bwd(const void* dy, const void* a, const void* res, const void*
                      void* da, void* dres, float* dgamma, float* dbeta, void* ws, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * Linear layers (P:410 Linear fusion through cuBLASLt; P:416 residual gradient through the
+ * GEMM's beta), row-major packed rows, bf16 activations / weights, fp32 accumulation:
+ *   ub_linear_fwd: y[T,N] = x[T,K] W[N,K]^T + b[N]    (b may be NULL; bias in the epilogue)
+ *   ub_linear_bwd: dx[T,K] = dy[T,N] W[N,K] (+ res_grad[T,K] if non-NULL, beta = 1);
+ *                  dW[N,K] = dy^T x (fp32), db[N] = sum_t dy (fp32, bias-gradient epilogue);
+ *                  dx or dW may be NULL to skip that GEMM; db needs dW.
+ * K, N multiples of 8; T >= 1 else UB_ERR_SHAPE.  ws: ub_linear_workspace_bytes() bytes
+ * (cuBLASLt workspace).  No algorithm for the shape -> UB_ERR_UNSUPPORTED. */
+size_t ub_linear_workspace_bytes(void);
+ub_status ub_linear_fwd(const void* x, const void* W, const void* b, int64_t T, int32_t K, int32_t N, void* y,
+                        void* ws, void* stream);
+ub_status ub_linear_bwd(const void* dy, const void* x, const void* W, const void* res_grad, int64_t T, int32_t K,
+                        int32_t N, void* dx, float* dW, float* db, void* ws, void* stream);
+
+/* ------------------------------------------------------------------------------------
+ * Unpadded encoder attention sub-layer (BASELINE config 4), packed rows:
+ *   qkv = x Wqkv^T + bqkv;  ctx = varlen_fmha(qkv) (p_attn, R5);  a = ctx Wo^T + bo;
+ *   y = LayerNorm(x + dropout(a)) (p_hidden, R21)
+ * Layouts: x, y, dy, dx, ctx, a [T, hidden] bf16; qkv [T, 3*hidden] bf16 (= [T, 3, H, 64]);
+ * Wqkv [3*hidden, hidden], Wo [hidden, hidden], bqkv [3*hidden], bo, gamma, beta [hidden]
+ * bf16; lse [H, T], mean, rstd [T] fp32; weight / bias / LN gradients fp32.  qkv, ctx, lse,
+ * a, mean, rstd are written by the forward and read by the backward (caller-owned).
+ * hidden / heads must be 64 and hidden <= 2048 (else UB_ERR_UNSUPPORTED).  ws:
+ * ub_encoder_attn_workspace_bytes(prm, is_bwd) bytes, 256-B aligned. */
+typedef struct {
+  int32_t B;          /* sequences */
+  int64_t T;          /* tokens = cu[B] */
+  int32_t max_seqlen;
+  int32_t hidden;     /* 1024 for BERT-large */
+  int32_t heads;      /* 16 for BERT-large */
+  float p_attn;       /* attention-probability dropout */
+  float p_hidden;     /* hidden dropout before the residual add */
+  float eps;          /* LayerNorm epsilon (1e-12 in BERT) */
+  uint64_t seed, offset;
+  int32_t num_ctas;   /* FMHA persistent grid, 0 = all SMs */
+} ub_encoder_params;
+size_t ub_encoder_attn_workspace_bytes(const ub_encoder_params* prm, int is_bwd);
+ub_status ub_encoder_attn_fwd(const ub_encoder_params* prm, const void* x, const int32_t* d_cu, const void* w_qkv,
+                              const void* b_qkv, const void* w_o, const void* b_o, const void* gamma,
+                              const void* beta, void* qkv, void* ctx, float* lse, void* a, float* mean, float* rstd,
+                              void* y, void* ws, void* stream);
+ub_status ub_encoder_attn_bwd(const ub_encoder_params* prm, const void* x, const int32_t* d_cu, const void* w_qkv,
+                              const void* w_o, const void* gamma, const void* qkv, const void* ctx, const float* lse,
+                              const void* a, const float* mean, const float* rstd, const void* dy, void* dx,
+                              float* dw_qkv, float* db_qkv, float* dw_o, float* db_o, float* dgamma, float* dbeta,
+                              void* ws, void* stream);
+
+/* ------------------------------------------------------------------------------------
  * Padding-exchange balancer (§IV-B-1).  Pure host function: deterministic,
  * byte-identical on every rank given the same all-gathered lengths.
  *   h_all_lengths [W*B]: rank-major all-gather of the valid lengths, global id g = r*B+k.

@@ -25,6 +25,11 @@ class FmhaParams(C.Structure):
                 ("num_ctas", i32)]
 
 
+class EncoderParams(C.Structure):
+    _fields_ = [("B", i32), ("T", i64), ("max_seqlen", i32), ("hidden", i32), ("heads", i32), ("p_attn", f32),
+                ("p_hidden", f32), ("eps", f32), ("seed", u64), ("offset", u64), ("num_ctas", i32)]
+
+
 SIGNATURES = {
     "ub_last_error": (C.c_char_p, []),
     "ub_version": (C.c_char_p, []),
@@ -39,6 +44,12 @@ SIGNATURES = {
     "ub_dal_fwd": (i32, [vp, vp, vp, vp, i64, i32, f32, f32, u64, u64, vp, vp, vp, vp]),
     "ub_dal_bwd_workspace_bytes": (sz, [i64, i32]),
     "ub_dal_bwd": (i32, [vp, vp, vp, vp, vp, vp, i64, i32, f32, u64, u64, vp, vp, vp, vp, vp, vp]),
+    "ub_linear_workspace_bytes": (sz, []),
+    "ub_linear_fwd": (i32, [vp, vp, vp, i64, i32, i32, vp, vp, vp]),
+    "ub_linear_bwd": (i32, [vp, vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp]),
+    "ub_encoder_attn_workspace_bytes": (sz, [C.POINTER(EncoderParams), C.c_int]),
+    "ub_encoder_attn_fwd": (i32, [C.POINTER(EncoderParams)] + [vp] * 17),
+    "ub_encoder_attn_bwd": (i32, [C.POINTER(EncoderParams)] + [vp] * 21),
     "ub_balance_plan": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp]),
     "ub_balance_plan_weighted": (i32, [vp, i32, i32, i32, i64, i64, vp, vp]),
     "ub_exchange_tables": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),

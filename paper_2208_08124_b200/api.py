@@ -12,7 +12,7 @@ import math
 import numpy as np
 import torch
 
-from ._lib import (UB_BAL_EXACT_SMALL, UB_BAL_LPT, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BF16, UB_FP32, FmhaParams, check, lib)
+from ._lib import (EncoderParams, UB_BAL_EXACT_SMALL, UB_BAL_LPT, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BF16, UB_FP32, FmhaParams, check, lib)
 
 BAL_MODES = {"paper": UB_BAL_PAPER, "snake": UB_BAL_SNAKE, "exact_small": UB_BAL_EXACT_SMALL, "lpt": UB_BAL_LPT}
 
@@ -164,6 +164,78 @@ def dal_bwd(dy: torch.Tensor, a: torch.Tensor, res: torch.Tensor, gamma: torch.T
                            float(p_dropout), int(seed), int(offset), _ptr(da), _ptr(dres), _ptr(dgamma), _ptr(dbeta),
                            _ptr(ws), _stream(stream)))
     return da, dres, dgamma, dbeta
+
+
+# ------------------------------------------------------------------ Linear (cuBLASLt) and the encoder sub-layer
+def linear_fwd(x: torch.Tensor, W: torch.Tensor, b: torch.Tensor | None = None, out=None, stream=None):
+    """y[T, N] = x[T, K] W[N, K]^T + b (P:410)."""
+    T, K = x.shape
+    N = W.shape[0]
+    y = out if out is not None else torch.empty((T, N), dtype=x.dtype, device=x.device)
+    ws = _workspace(lib().ub_linear_workspace_bytes(), x.device, "linear")
+    check(lib().ub_linear_fwd(_ptr(x), _ptr(W), _ptr(b), int(T), int(K), int(N), _ptr(y), _ptr(ws), _stream(stream)))
+    return y
+
+
+def linear_bwd(dy: torch.Tensor, x: torch.Tensor, W: torch.Tensor, res_grad: torch.Tensor | None = None, stream=None):
+    """(dx = dy W (+ res_grad), dW = dy^T x (fp32), db = sum_t dy (fp32)) -- P:410."""
+    T, N = dy.shape
+    K = W.shape[1]
+    dx = torch.empty((T, K), dtype=dy.dtype, device=dy.device)
+    dW = torch.empty((N, K), dtype=torch.float32, device=dy.device)
+    db = torch.empty(N, dtype=torch.float32, device=dy.device)
+    ws = _workspace(lib().ub_linear_workspace_bytes(), dy.device, "linear")
+    check(lib().ub_linear_bwd(_ptr(dy), _ptr(x), _ptr(W), _ptr(res_grad), int(T), int(K), int(N), _ptr(dx), _ptr(dW),
+                              _ptr(db), _ptr(ws), _stream(stream)))
+    return dx, dW, db
+
+
+def encoder_params(B, T, max_seqlen, hidden=1024, heads=16, p_attn=0.0, p_hidden=0.0, eps=1e-12, seed=0, offset=0,
+                   num_ctas=0):
+    return EncoderParams(B=int(B), T=int(T), max_seqlen=int(max_seqlen), hidden=int(hidden), heads=int(heads),
+                         p_attn=float(p_attn), p_hidden=float(p_hidden), eps=float(eps), seed=int(seed),
+                         offset=int(offset), num_ctas=int(num_ctas))
+
+
+def encoder_attn_fwd(x, cu, max_seqlen, w_qkv, b_qkv, w_o, b_o, gamma, beta, heads=16, p_attn=0.0, p_hidden=0.0,
+                     eps=1e-12, seed=0, offset=0, saved=None, out=None, stream=None, num_ctas=0):
+    """Unpadded encoder attention sub-layer forward (NEXT-1): returns (y, saved) where saved
+    holds the activations the backward reads (qkv, ctx, lse, a, mean, rstd)."""
+    T, hid = x.shape
+    prm = encoder_params(cu.numel() - 1, T, max_seqlen, hid, heads, p_attn, p_hidden, eps, seed, offset, num_ctas)
+    dev = x.device
+    if saved is None:
+        saved = {"qkv": torch.empty((T, 3 * hid), dtype=x.dtype, device=dev),
+                 "ctx": torch.empty((T, hid), dtype=x.dtype, device=dev),
+                 "lse": torch.empty((heads, T), dtype=torch.float32, device=dev),
+                 "a": torch.empty((T, hid), dtype=x.dtype, device=dev),
+                 "mean": torch.empty(T, dtype=torch.float32, device=dev),
+                 "rstd": torch.empty(T, dtype=torch.float32, device=dev)}
+    y = out if out is not None else torch.empty_like(x)
+    ws = _workspace(lib().ub_encoder_attn_workspace_bytes(C.byref(prm), 0), dev, "encoder_fwd")
+    check(lib().ub_encoder_attn_fwd(C.byref(prm), _ptr(x), _ptr(cu), _ptr(w_qkv), _ptr(b_qkv), _ptr(w_o), _ptr(b_o),
+                                    _ptr(gamma), _ptr(beta), _ptr(saved["qkv"]), _ptr(saved["ctx"]), _ptr(saved["lse"]),
+                                    _ptr(saved["a"]), _ptr(saved["mean"]), _ptr(saved["rstd"]), _ptr(y), _ptr(ws),
+                                    _stream(stream)))
+    return y, saved
+
+
+def encoder_attn_bwd(dy, x, cu, max_seqlen, w_qkv, w_o, gamma, saved, heads=16, p_attn=0.0, p_hidden=0.0, eps=1e-12,
+                     seed=0, offset=0, stream=None, num_ctas=0):
+    """Backward of encoder_attn_fwd: returns dict dx, dw_qkv, db_qkv, dw_o, db_o, dgamma, dbeta."""
+    T, hid = x.shape
+    prm = encoder_params(cu.numel() - 1, T, max_seqlen, hid, heads, p_attn, p_hidden, eps, seed, offset, num_ctas)
+    dev = x.device
+    f32 = lambda *shape: torch.empty(shape, dtype=torch.float32, device=dev)
+    g = {"dx": torch.empty_like(x), "dw_qkv": f32(3 * hid, hid), "db_qkv": f32(3 * hid), "dw_o": f32(hid, hid),
+         "db_o": f32(hid), "dgamma": f32(hid), "dbeta": f32(hid)}
+    ws = _workspace(lib().ub_encoder_attn_workspace_bytes(C.byref(prm), 1), dev, "encoder_bwd")
+    check(lib().ub_encoder_attn_bwd(C.byref(prm), _ptr(x), _ptr(cu), _ptr(w_qkv), _ptr(w_o), _ptr(gamma),
+                                    _ptr(saved["qkv"]), _ptr(saved["ctx"]), _ptr(saved["lse"]), _ptr(saved["a"]),
+                                    _ptr(saved["mean"]), _ptr(saved["rstd"]), _ptr(dy), _ptr(g["dx"]), _ptr(g["dw_qkv"]),
+                                    _ptr(g["db_qkv"]), _ptr(g["dw_o"]), _ptr(g["db_o"]), _ptr(g["dgamma"]),
+                                    _ptr(g["dbeta"]), _ptr(ws), _stream(stream)))
+    return g
 
 
 # ------------------------------------------------------------------ balancer

@@ -21,6 +21,19 @@ def _nccl_dir() -> str:
     return os.path.dirname(nvidia.nccl.__file__) if nvidia.nccl.__file__ else list(nvidia.nccl.__path__)[0]
 
 
+def _cublas_dir() -> str:
+    """cuBLASLt for the encoder's plain GEMMs: the torch-bundled copy (the one torch itself
+    loads into the process), else the toolkit's."""
+    try:
+        import nvidia.cublas
+        d = os.path.join(list(nvidia.cublas.__path__)[0], "lib")
+        if os.path.exists(os.path.join(d, "libcublasLt.so.12")):
+            return d
+    except ImportError:
+        pass
+    return "/usr/local/cuda/lib64"
+
+
 def _flags():
     nccl = _nccl_dir()
     return nccl, ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -73,9 +86,11 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
     if force or jobs or _stale(lib, objs):
         nccl_lib = os.path.join(nccl, "lib")
         # export only the C ABI (ub_*): visibility=hidden + explicit default in ub.h users
+        blas_lib = _cublas_dir()
         cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + [
-            "-L" + nccl_lib, "-l:libnccl.so.2", "-lcudart",
-            "-Xlinker", "-rpath," + nccl_lib, "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")]
+            "-L" + nccl_lib, "-l:libnccl.so.2", "-L" + blas_lib, "-l:libcublasLt.so.12", "-lcudart",
+            "-Xlinker", "-rpath," + nccl_lib, "-Xlinker", "-rpath," + blas_lib,
+            "-Xlinker", "--version-script=" + os.path.join(CSRC, "exports.map")]
         run(cmd)
     return lib
 
