@@ -15,10 +15,10 @@ Forward, for each sequence b (length L) and head h:
     S[:, j >= L] = -inf                      (padding keys masked)
     m_i = max_j S_ij ;  l_i = sum_j exp(S_ij - m_i)
     P   = exp(S - m) / l ;   LSE_i = m_i + log l_i
-    Pd  = P * M / (1 - p)   if p > 0 else P  (M = keep mask)
+    Pd  = P * M * r         if p > 0 else P  (M = keep mask, r = 1 / (1 - floor(256 p) / 256), R5)
     O   = Pd V ;  O[i >= L] = 0
 Backward (chain rule through the same steps):
-    dV  = Pd^T dO ;  dPd = dO V^T ;  dP = dPd * M / (1 - p)
+    dV  = Pd^T dO ;  dPd = dO V^T ;  dP = dPd * M * r
     Delta_i = sum_j P_ij dP_ij  (= sum_d dO_id O_id)
     dS  = P * (dP - Delta)      ;  dQ = scale * dS K ;  dK = scale * dS^T Q
 
@@ -66,7 +66,7 @@ def mha_fwd_padded(q, k, v, lengths, scale, p=0.0, keep=None):
             LSE[b, h, :L] = (m + np.log(l))[:L, 0]
             if p > 0.0:
                 M = _keep_full(keep(b, h), L, S)
-                P = P * M / (1.0 - p)
+                P = P * M * philox.dropout_scale(p)
             Ob = P @ v[b, :, h, :]
             Ob[L:, :] = 0.0
             O[b, :, h, :] = Ob
@@ -90,7 +90,7 @@ def mha_bwd_padded(q, k, v, dout, lengths, scale, p=0.0, keep=None):
             P[L:, :] = 0.0                      # padded query rows produce nothing (R3)
             if p > 0.0:
                 M = _keep_full(keep(b, h), L, S)
-                Pd = P * M / (1.0 - p)
+                Pd = P * M * philox.dropout_scale(p)
             else:
                 M = None
                 Pd = P
@@ -98,7 +98,7 @@ def mha_bwd_padded(q, k, v, dout, lengths, scale, p=0.0, keep=None):
             dO[L:, :] = 0.0
             dV[b, :, h, :] = Pd.T @ dO
             dPd = dO @ v[b, :, h, :].T
-            dP = dPd * M / (1.0 - p) if p > 0.0 else dPd
+            dP = dPd * M * philox.dropout_scale(p) if p > 0.0 else dPd
             Delta = np.sum(P * dP, axis=1, keepdims=True)
             dS = P * (dP - Delta)
             dQ[b, :, h, :] = scale * (dS @ k[b, :, h, :])

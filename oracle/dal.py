@@ -28,7 +28,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .philox import MASK32, dropout_threshold, philox4x32_10
+from .philox import MASK32, philox4x32_10
 
 DAL_SALT = 0xDA100000
 
@@ -37,7 +37,7 @@ def dal_keep_mask(seed: int, offset: int, T: int, E: int, p: float) -> np.ndarra
     """keep[t, col] (bool) for rows 0..T-1, columns 0..E-1 -- R21."""
     if p <= 0.0:
         return np.ones((T, E), dtype=bool)
-    thr = dropout_threshold(p)
+    thr = int(np.floor(float(np.float32(p)) * 65536.0))      # 16-bit decisions (R21)
     t = np.arange(T, dtype=np.uint64)[:, None]
     c = np.arange(E, dtype=np.uint64)[None, :]
     tt, cc = np.broadcast_arrays(t, c)
