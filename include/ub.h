@@ -98,7 +98,8 @@ ub_status ub_pad(const void* packed, void* padded, const int32_t* d_cu, int32_t 
  *     O = softmax(scale * Q K^T) V   per sequence b and head h, within the sequence only
  * (unpadded FMHA over packed tokens; no cross-sequence attention, R2), with
  * optional inverted dropout on the probabilities (R4) from the counter-based Philox
- * mask of R5 keyed by (seed, offset).
+ * mask of R5 keyed by (seed, offset): 8-bit decisions, 16 keys per Philox call, p quantised to
+ * floor(256 p) / 256 and kept values scaled by the exact inverse keep probability.
  *
  * Work is grouped by length: a device-side plan buckets sequences by their number of
  * 128-token tiles -- the paper's groups (0,128] (128,256] (256,384] (384,512]

@@ -104,17 +104,18 @@ constexpr uint32_t kIdescS = idesc_bf16_f32(128, 128, 0, 0);     // S^T, dP^T: K
 constexpr uint32_t kIdescTS = idesc_bf16_f32(128, 64, 0, 1);     // dV, dK: A in TMEM, B MN-major
 constexpr uint32_t kIdescQ = idesc_bf16_f32(128, 64, 1, 1);      // dQ: A MN-major, B MN-major
 
-// keep bits of 8 query columns [q0, q0+8) for this thread's key (lane-cooperative Philox):
-// lane l computes the mask word of key group (l/8) at column q0 + (l%8); lanes then gather
-// bit (l%8) of their group's 8 words.
-__device__ __forceinline__ uint32_t keep8_cols(uint32_t key_grp_j0, uint32_t t_q0, uint32_t h, const Params& prm,
-                                               uint32_t lane) {
-  const uint32_t word = keep_bits8(key_grp_j0, t_q0 + (lane & 7), h, prm.off, prm.k0, prm.k1, prm.thr);
+// keep bits of 16 query columns [q0, q0+16) for this thread's key (lane-cooperative Philox):
+// the warp's 32 keys are two 16-key Philox blocks; lane l computes the block (l / 16) word
+// set of query column q0 + (l % 16), then every lane gathers bit (l % 16) of the 16 words of
+// its block.
+__device__ __forceinline__ uint32_t keep16_cols(uint32_t warp_j0, uint32_t t_q0, uint32_t h, const Params& prm,
+                                                uint32_t lane) {
+  const uint32_t word = keep_bits16(warp_j0 + (lane & 16u), t_q0 + (lane & 15u), h, prm.off, prm.k0, prm.k1, prm.thr);
   uint32_t bits = 0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const uint32_t w = __shfl_sync(0xffffffffu, word, (lane & ~7u) + k);
-    bits |= ((w >> (lane & 7)) & 1u) << k;
+  for (int k = 0; k < 16; ++k) {
+    const uint32_t w = __shfl_sync(0xffffffffu, word, (lane & 16u) + k);
+    bits |= ((w >> (lane & 15u)) & 1u) << k;
   }
   return bits;
 }
@@ -325,7 +326,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       for (int32_t kt = 0; kt < it.nt; ++kt) {
         const int32_t key = kt * kTile + (int32_t)r;
         const bool key_ok = key < it.L;
-        const uint32_t grp_j0 = (uint32_t)(kt * kTile) + (warp & 3) * 32 + (lane & ~7u);
+        const uint32_t warp_j0 = (uint32_t)(kt * kTile) + (warp & 3) * 32;   // the warp's first key
         for (int32_t i = 0; i < it.nt; ++i, ++qit) {
           const uint32_t st = qit % kQStages;
           const int32_t qvalid = it.L - i * kTile;          // query rows of this tile inside the sequence
@@ -355,7 +356,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
               keep = 0;
               const uint32_t tq = (uint32_t)(it.c0 + i * kTile + q0);
 #pragma unroll
-              for (int b8 = 0; b8 < 4; ++b8) keep |= keep8_cols(grp_j0, tq + 8 * b8, it.h, prm, lane) << (8 * b8);
+              for (int b16 = 0; b16 < 2; ++b16) keep |= keep16_cols(warp_j0, tq + 16 * b16, it.h, prm, lane) << (16 * b16);
             }
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
@@ -677,8 +678,8 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   prm.T = p.T;
   prm.scale = p.scale;
   prm.scale_log2 = p.scale * 1.4426950408889634f;
-  prm.rp = 1.f / (1.f - p.p_dropout);
-  prm.thr = drop ? (uint32_t)floor((double)p.p_dropout * 65536.0) : 0u;
+  prm.thr = drop ? (uint32_t)floor((double)p.p_dropout * 256.0) : 0u;   // R5: 8-bit decisions
+  prm.rp = 1.f / (1.f - (float)prm.thr / 256.f);
   prm.k0 = (uint32_t)(p.seed & 0xFFFFFFFFull);
   prm.k1 = (uint32_t)(p.seed >> 32);
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);

@@ -142,18 +142,15 @@ __device__ __forceinline__ int32_t snake_item(int32_t r, int32_t c, int32_t G) {
   return r * G + ((r & 1) ? (G - 1 - c) : c);
 }
 
-// Dropout keep bits for 8 consecutive keys j0..j0+7 (j0 % 8 == 0) of packed row t (R5):
-// bit e set <=> key j0+e kept.
-__device__ __forceinline__ uint32_t keep_bits8(uint32_t j0, uint32_t t, uint32_t h, uint32_t off, uint32_t k0,
-                                               uint32_t k1, uint32_t thr) {
-  const U4 w = philox4x32_10(j0 >> 3, t, h, off, k0, k1);
+// Dropout keep bits for 16 consecutive keys j0..j0+15 (j0 % 16 == 0) of packed row t (R5):
+// bit e set <=> byte e of the Philox block (word e >> 2, byte e & 3) >= thr (8-bit threshold).
+__device__ __forceinline__ uint32_t keep_bits16(uint32_t j0, uint32_t t, uint32_t h, uint32_t off, uint32_t k0,
+                                                uint32_t k1, uint32_t thr) {
+  const U4 w = philox4x32_10(j0 >> 4, t, h, off, k0, k1);
   const uint32_t words[4] = {w.x, w.y, w.z, w.w};
   uint32_t bits = 0;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const uint32_t r16 = (words[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-    bits |= (r16 >= thr ? 1u : 0u) << e;
-  }
+  for (int e = 0; e < 16; ++e) bits |= (((words[e >> 2] >> (8 * (e & 3))) & 0xFFu) >= thr ? 1u : 0u) << e;
   return bits;
 }
 

@@ -377,6 +377,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         const uint64_t neg2 = f2pack(negm, negm);
         uint64_t acc2[4] = {0, 0, 0, 0};
         uint32_t pk[kTile / 2];
+        uint32_t bits16 = 0;
         if (kExpTurns) named_bar_sync(1 + x, 256);     // my turn for the exp phase
 #pragma unroll
         for (int g = 0; g < kTile / 8; ++g) {          // 8 keys at a time: exp2, sum, dropout, pack
@@ -397,7 +398,8 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             e8[2 * u + 1] = b;
           }
           if (kDropout) {
-            const uint32_t bits = keep_bits8(j * kTile + g * 8, t_glob, it.h, prm.off, prm.k0, prm.k1, prm.thr);
+            if ((g & 1) == 0) bits16 = keep_bits16(j * kTile + g * 8, t_glob, it.h, prm.off, prm.k0, prm.k1, prm.thr);
+            const uint32_t bits = bits16 >> (8 * (g & 1));
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               if (!((bits >> e) & 1u)) e8[e] = 0.f;
@@ -533,8 +535,8 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   prm.T = p.T;
   prm.scale = p.scale;
   prm.scale_log2 = p.scale * 1.4426950408889634f;
-  prm.rp = 1.f / (1.f - p.p_dropout);
-  prm.thr = p.p_dropout > 0.f ? (uint32_t)floor((double)p.p_dropout * 65536.0) : 0u;
+  prm.thr = p.p_dropout > 0.f ? (uint32_t)floor((double)p.p_dropout * 256.0) : 0u;   // R5: 8-bit decisions
+  prm.rp = 1.f / (1.f - (float)prm.thr / 256.f);                                       // exact keep probability
   prm.k0 = (uint32_t)(p.seed & 0xFFFFFFFFull);
   prm.k1 = (uint32_t)(p.seed >> 32);
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);

@@ -15,16 +15,16 @@ constexpr int kMaxD = 128;
 struct SimtArgs {
   const float* qkv; const int32_t* cu; float* out; float* lse; const float* dout; const float* o;
   float* dqkv; float* delta;
-  int32_t H, D; int64_t T; float scale, p; uint32_t thr, k0, k1, off;
+  int32_t H, D; int64_t T; float scale, p, rp; uint32_t thr, k0, k1, off;
 };
 
 __device__ __forceinline__ bool keep_elem(const SimtArgs& a, int64_t t, int h, int j) {
   if (a.thr == 0) return true;
-  const U4 w = philox4x32_10((uint32_t)j >> 3, (uint32_t)t, (uint32_t)h, a.off, a.k0, a.k1);
-  const int widx = (j & 7) >> 1;
+  const U4 w = philox4x32_10((uint32_t)j >> 4, (uint32_t)t, (uint32_t)h, a.off, a.k0, a.k1);
+  const int widx = (j & 15) >> 2;
   const uint32_t word = widx == 0 ? w.x : widx == 1 ? w.y : widx == 2 ? w.z : w.w;
-  const uint32_t r16 = (word >> (16 * (j & 1))) & 0xFFFFu;
-  return r16 >= a.thr;
+  const uint32_t r8 = (word >> (8 * (j & 3))) & 0xFFu;
+  return r8 >= a.thr;
 }
 
 __device__ __forceinline__ const float* row_ptr(const SimtArgs& a, int64_t t, int which, int h) {
@@ -59,7 +59,7 @@ __global__ void simt_fwd_kernel(SimtArgs a) {
       for (int d = 0; d < a.D; ++d) acc[d] = fmaf(pexp, vp[d], acc[d]);
     }
   }
-  const float inv = 1.f / (l * (1.f - a.p));
+  const float inv = a.rp / l;
   float* op = a.out + (t * a.H + h) * (int64_t)a.D;
   for (int d = 0; d < a.D; ++d) op[d] = acc[d] * inv;
   a.lse[(int64_t)h * a.T + t] = m + logf(l);
@@ -89,7 +89,7 @@ __global__ void simt_dq_kernel(SimtArgs a) {
   const float* gp = a.dout + (t * a.H + h) * (int64_t)a.D;
   for (int d = 0; d < a.D; ++d) { q[d] = qp[d]; g[d] = gp[d]; acc[d] = 0.f; }
   const float lse = a.lse[(int64_t)h * a.T + t], dl = a.delta[(int64_t)h * a.T + t];
-  const float rs = 1.f / (1.f - a.p);
+  const float rs = a.rp;
   for (int j = 0; j < L; ++j) {
     const float* kp = row_ptr(a, c0 + j, 1, h);
     const float* vp = row_ptr(a, c0 + j, 2, h);
@@ -115,7 +115,7 @@ __global__ void simt_dkdv_kernel(SimtArgs a) {
   const float* kp = row_ptr(a, tj, 1, h);
   const float* vp = row_ptr(a, tj, 2, h);
   for (int d = 0; d < a.D; ++d) { k[d] = kp[d]; v[d] = vp[d]; dk[d] = 0.f; dv[d] = 0.f; }
-  const float rs = 1.f / (1.f - a.p);
+  const float rs = a.rp;
   for (int i = 0; i < L; ++i) {
     const int64_t ti = c0 + i;
     const float* qp = row_ptr(a, ti, 0, h);
@@ -137,7 +137,8 @@ __global__ void simt_dkdv_kernel(SimtArgs a) {
 static SimtArgs make_args(const ub_fmha_params& p) {
   SimtArgs a{};
   a.H = p.heads; a.D = p.head_dim; a.T = p.T; a.scale = p.scale; a.p = p.p_dropout;
-  a.thr = p.p_dropout > 0.f ? (uint32_t)floor((double)p.p_dropout * 65536.0) : 0u;
+  a.thr = p.p_dropout > 0.f ? (uint32_t)floor((double)p.p_dropout * 256.0) : 0u;   // R5: 8-bit decisions
+  a.rp = 1.f / (1.f - (float)a.thr / 256.f);
   a.k0 = (uint32_t)(p.seed & 0xFFFFFFFFull); a.k1 = (uint32_t)(p.seed >> 32);
   a.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
   return a;

@@ -1,7 +1,7 @@
 """Dev probe: fwd/bwd timing at BERT-large config 2 (not a bench number).
 Reports the whole call and the main kernel alone (library profile events)."""
 import sys
-sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
+import os; _R = os.environ.get("UB_ROOT", "/root/repo"); sys.path.insert(0, _R); sys.path.insert(0, _R + "/tests")
 import numpy as np, torch
 import paper_2208_08124_b200 as ub
 import synth
