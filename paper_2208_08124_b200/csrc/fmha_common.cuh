@@ -148,9 +148,14 @@ __device__ __forceinline__ uint32_t keep_bits16(uint32_t j0, uint32_t t, uint32_
                                                 uint32_t k1, uint32_t thr) {
   const U4 w = philox4x32_10(j0 >> 4, t, h, off, k0, k1);
   const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+  const uint32_t t4 = thr * 0x01010101u;
   uint32_t bits = 0;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) bits |= (((words[e >> 2] >> (8 * (e & 3))) & 0xFFu) >= thr ? 1u : 0u) << e;
+  for (int q = 0; q < 4; ++q) {
+    // bytewise r8 >= thr (0xFF / 0x00 per byte), one distinct bit per byte, summed by a multiply
+    const uint32_t m = __vcmpgeu4(words[q], t4) & 0x08040201u;
+    bits |= ((m * 0x01010101u) >> 24) << (4 * q);
+  }
   return bits;
 }
 
