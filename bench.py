@@ -474,6 +474,7 @@ def run_ours(args, world, rank, local):
     e2e = None if args.no_e2e else run_e2e(args, wl, world)
     gather = gather_bench(wl, peaks) if rank == 0 else None
     encoder = encoder_bench(wl, peaks) if rank == 0 and not args.no_encoder else None
+    drop01 = dropout_bench(wl) if rank == 0 and args.p_dropout == 0.0 else None
     out = {"metric": "unpadded FMHA fwd+bwd tokens/s (BERT-large)", "value": round(value, 1), "unit": "tokens/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -484,7 +485,8 @@ def run_ours(args, world, rank, local):
                       "step": "unpad records + exchange (side stream) | fmha fwd + bwd + pad (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
-           "main_stream_timeline": timeline, "gather": gather, "encoder_attn_sublayer": encoder, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
+           "main_stream_timeline": timeline, "attn_dropout_0.1": drop01, "gather": gather,
+           "encoder_attn_sublayer": encoder, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
            "host_us_per_step": dict(zip(["step_setup", "fwd_call", "bwd_call", "pad_call", "unpad_call", "finish_call",
                                               "begin_call"],
                                         [round(1e6 * float(x), 1) for x in np.median(np.array(marks), axis=0)]),
@@ -550,6 +552,34 @@ def gather_bench(wl, peaks, iters=20):
         out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
                      "bytes": int(nbytes), "p_dropout": 0.1}
     return out
+
+
+def dropout_bench(wl, iters=10):
+    """The same FMHA fwd + bwd at attention dropout p = 0.1 (BERT-large's training value,
+    SURVEY §8(d)), device time of the main kernels from the library's events."""
+    from paper_2208_08124_b200 import api
+    ub = wl.ub
+    st, ex = wl.sets[0], wl.ex[0]
+    T = ex["T"]
+    qkv, dout = st["qkv"][:T], st["dout"][:T]
+    cu = ex["cu"]
+    o, lse = ub.varlen_fmha_fwd(qkv, cu, S, None, 0.1, 7, 0)
+    res = {}
+    for name, kid, fn in (("fwd", api.PROF_FWD, lambda: ub.varlen_fmha_fwd(qkv, cu, S, None, 0.1, 7, 0, out=o, lse=lse)),
+                          ("bwd", api.PROF_BWD, lambda: ub.varlen_fmha_bwd(qkv, o, lse, dout, cu, S, None, 0.1, 7, 0))):
+        fn()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        for k in range(iters):
+            api.profile_events(kid, *ev[k])
+            fn()
+        api.profile_events(kid)
+        torch.cuda.synchronize()
+        res[name + "_us"] = round(float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3, 2)
+    res["fmha_only_tokens_per_s"] = round(T / ((res["fwd_us"] + res["bwd_us"]) * 1e-6), 1)
+    res["note"] = "main kernels only, L2-warm single batch; headline runs p = 0 (config 2 names no dropout)"
+    return res
 
 
 def encoder_bench(wl, peaks, iters=10):
