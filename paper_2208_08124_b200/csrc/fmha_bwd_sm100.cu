@@ -136,6 +136,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   uint32_t tr_n = 0;
   (void)tr_n;
 
+  pdl_launch_dependents();
   if (warp == 12 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
     tma_prefetch_desc(&tmap_do);
@@ -158,8 +159,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     mbar_init(&sm.dkv_free, 4);
     fence_mbar_init();
   }
-  if (!kBigB && warp == 12) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 0, lane);
   if (warp == 13) tmem_alloc(&sm.tmem_base, 512);
+  pdl_wait();                                            // everything below may read / write global memory
+  if (!kBigB && warp == 12) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 0, lane);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -597,6 +599,8 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ out,
                                                       const __nv_bfloat16* __restrict__ dout, float* __restrict__ delta,
                                                       int64_t T, int32_t H) {
+  pdl_launch_dependents();
+  pdl_wait();                                      // O comes from the forward
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t row = gtid >> 3;                   // (t, h) row
   const int part = (int)(gtid & 7);
@@ -661,8 +665,8 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
   if (p.B > kPlanCap && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 0, v, s)) != UB_OK) return st;
   const int64_t rows = p.T * p.heads;
-  bwd::bwd_pre_kernel<<<(unsigned)((rows * 8 + 255) / 256), 256, 0, s>>>(
-      static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), delta, p.T, p.heads);
+  launch_pdl(bwd::bwd_pre_kernel, dim3((unsigned)((rows * 8 + 255) / 256)), dim3(256), 0, s,
+             static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), delta, p.T, p.heads);
   UB_CHECK_LAUNCH();
 
   bwd::Params prm{};
@@ -690,7 +694,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfBwd, 0, s);
-  kern<<<grid, bwd::kThreads, bwd::kSmemBytes, s>>>(tq, tdo, tdq, tdkv, prm);
+  launch_pdl(kern, dim3(grid), dim3(bwd::kThreads), bwd::kSmemBytes, s, tq, tdo, tdq, tdkv, prm);
   UB_CHECK_LAUNCH();
   prof_record(kProfBwd, 1, s);
   return UB_OK;

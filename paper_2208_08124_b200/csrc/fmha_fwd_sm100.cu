@@ -114,6 +114,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   uint32_t tr_n = 0;
   (void)tr_n;
 
+  pdl_launch_dependents();
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
     tma_prefetch_desc(&tmap_out);
@@ -132,8 +133,9 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     }
     fence_mbar_init();
   }
-  if (!kBigB && warp == 8) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 2, lane);
   if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
+  pdl_wait();                                            // everything below may read / write global memory
+  if (!kBigB && warp == 8) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 2, lane);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -548,7 +550,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfFwd, 0, s);
-  kern<<<grid, fwd::kThreads, fwd::kSmemBytes, s>>>(tmap, tmap_out, prm);
+  launch_pdl(kern, dim3(grid), dim3(fwd::kThreads), fwd::kSmemBytes, s, tmap, tmap_out, prm);
   UB_CHECK_LAUNCH();
   prof_record(kProfFwd, 1, s);
   return UB_OK;

@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <utility>
 
 #include "../../include/ub.h"
 
@@ -72,5 +73,25 @@ ub_status fmha_bwd_simt(const ub_fmha_params& p, const float* qkv, const float* 
                         const float* dout, const int32_t* d_cu, float* dqkv, float* ws, cudaStream_t s);
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Programmatic dependent launch (sm_90+): the kernel may be scheduled while the previous
+// kernel in the stream drains; it calls pdl_wait() before touching memory that kernel (or
+// anything ordered before it) produces.  Hides the launch latency and the prologue (barrier
+// init, TMEM allocation) behind the previous kernel's tail.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace ub

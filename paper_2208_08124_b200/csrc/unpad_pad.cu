@@ -6,6 +6,7 @@
 // coalesced, packed-side accesses are contiguous within each row.  Row -> (b, i) uses
 // multiply-high division (no integer divide on the hot loop).  16-B vectors when the
 // row and both base pointers allow it.
+#include "sm100.cuh"
 #include "ub_internal.h"
 
 namespace ub {
@@ -84,6 +85,8 @@ __global__ void __launch_bounds__(kSpanThreads) span_copy_kernel(const int4* __r
                                                                  const int32_t* __restrict__ cu, const int4* __restrict__ pad_row,
                                                                  int32_t B, int32_t S, int64_t V, int64_t n_copy,
                                                                  int64_t n_zero, int32_t copy_ctas) {
+  pdl_launch_dependents();
+  pdl_wait();                                      // the source rows may come from the previous kernel
   const bool zero = kPad && (int32_t)blockIdx.x >= copy_ctas;
   const int64_t n = zero ? n_zero : n_copy;
   const int64_t beg = (int64_t)(zero ? blockIdx.x - copy_ctas : blockIdx.x) * kSpanVecs;
@@ -139,12 +142,11 @@ static ub_status launch_span(bool pad, const void* src, void* dst, const int32_t
   const int pk = pad ? kProfPad : kProfUnpad;
   prof_record(pk, 0, s);
   if (pad)
-    span_copy_kernel<true><<<(unsigned)(cc + zc), kSpanThreads, 0, s>>>(
-        static_cast<const int4*>(src), static_cast<int4*>(dst), d_cu, static_cast<const int4*>(pad_row), B, S, V, n_copy,
-        n_zero, (int32_t)cc);
+    launch_pdl(span_copy_kernel<true>, dim3((unsigned)(cc + zc)), dim3(kSpanThreads), 0, s, static_cast<const int4*>(src),
+               static_cast<int4*>(dst), d_cu, static_cast<const int4*>(pad_row), B, S, V, n_copy, n_zero, (int32_t)cc);
   else
-    span_copy_kernel<false><<<(unsigned)cc, kSpanThreads, 0, s>>>(static_cast<const int4*>(src), static_cast<int4*>(dst),
-                                                                   d_cu, nullptr, B, S, V, n_copy, 0, (int32_t)cc);
+    launch_pdl(span_copy_kernel<false>, dim3((unsigned)cc), dim3(kSpanThreads), 0, s, static_cast<const int4*>(src),
+               static_cast<int4*>(dst), d_cu, static_cast<const int4*>(nullptr), B, S, V, n_copy, (int64_t)0, (int32_t)cc);
   UB_CHECK_LAUNCH();
   prof_record(pk, 1, s);
   return UB_OK;
