@@ -11,8 +11,9 @@ per GPU (H=16, D=64, max_seqlen 512, MLPerf-like length mix, bf16):
                ncclSend/ncclRecv, reorder, cu_seqlens H2D
   main stream:
     a7 varlen FMHA forward over the exchanged cu_seqlens
+    a9 pad     attention output [T, 1024] -> [56, 512, 1024], fused into a7's
+               epilogue (ub_varlen_fmha_fwd_pad; zeros past each length)
     a8 varlen FMHA backward (dO given)
-    a9 pad     attention output [T, 1024] -> [56, 512, 1024]
 Metric (BASELINE.json): unpadded FMHA fwd+bwd tokens/s, with the roofline fraction of the
 dominant kernel and the 8-GPU token imbalance.
 
@@ -45,7 +46,7 @@ SREC = 4      # per-sample record: next_sentence_label (int32)
 N_SETS = 3    # rotating input sets: each step's working set (> 300 MB) and the 2 others exceed L2
 N_EX = 4      # exchange output buffers in flight: the side stream never waits on the step just enqueued
 PIPE = 2      # step n computes while step n+PIPE is exchanged and n+PIPE+1's lengths are gathered
-KERNELS_PER_STEP = 7    # ours: unpad, 2x exchange copy, fwd main, bwd pre (Delta) + main, pad
+KERNELS_PER_STEP = 6    # ours: unpad, 2x exchange copy, fwd main (+ fused pad), bwd pre (Delta) + main
 
 
 def parse():
@@ -356,15 +357,16 @@ class Workload:
         if marks is not None:
             marks.append(time.perf_counter())
         qkv, out = self.view(st, "qkv", T), self.view(self, "out", T)
+        # a7 + a9: the forward's epilogue also writes the padded copy of O, zeros past
+        # each length -- the separate pad pass is gone (ub_varlen_fmha_fwd_pad)
         self.ub.varlen_fmha_fwd(qkv, ex["cu"], S, None, p, 0x2208 + n, 0, out=out, lse=self.lse, num_ctas=self.ctas,
-                                stream=self.main)
+                                stream=self.main, padded=self.padded_out)
         if marks is not None:
             marks.append(time.perf_counter())
         self.ub.varlen_fmha_bwd(qkv, out, self.lse, self.view(st, "dout", T), ex["cu"], S, None, p, 0x2208 + n, 0,
                                 dqkv=self.view(self, "dqkv", T), num_ctas=self.ctas, stream=self.main)
         if marks is not None:
             marks.append(time.perf_counter())
-        self.ub.pad(out, ex["cu"], B, S, out=self.padded_out, stream=self.main)
         self.done[n % N_EX].record(self.main)
         if marks is not None:
             marks.append(time.perf_counter())
@@ -390,7 +392,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     barrier(world)
     # timed region
-    kids = [ub.api.PROF_FWD, ub.api.PROF_BWD, ub.api.PROF_PAD, ub.api.PROF_UNPAD]
+    kids = [ub.api.PROF_FWD, ub.api.PROF_BWD, ub.api.PROF_UNPAD]
     prof_events = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in kids}
                    for _ in range(args.steps)]
     for d in prof_events:                 # create the cudaEvent_t handles outside the timed loop
@@ -441,12 +443,10 @@ def run_ours(args, world, rank, local):
     f_fwd = [flops_fwd(L) for L in lens_used]
     f_bwd = [flops_bwd(L) for L in lens_used]
     fwd_us, bwd_us = np.mean(kt[kids[0]]) * 1e3, np.mean(kt[kids[1]]) * 1e3
-    pad_us, unpad_us = np.mean(kt[kids[2]]) * 1e3, np.mean(kt[kids[3]]) * 1e3
+    unpad_us = np.mean(kt[kids[2]]) * 1e3
     fwd_tf = np.mean(f_fwd) / (fwd_us * 1e-6) / 1e12
     bwd_tf = np.mean(f_bwd) / (bwd_us * 1e-6) / 1e12
     mean_T = tokens / args.steps
-    pad_bytes = mean_T * H * D * 2 + B * S * H * D * 2
-    pad_gbs = pad_bytes / (pad_us * 1e-6) / 1e9
     peak_tc = peaks["bf16_sust"] or peaks["bf16"]
     dom = "bwd" if bwd_us >= fwd_us else "fwd"
     achieved = bwd_tf if dom == "bwd" else fwd_tf
@@ -458,18 +458,17 @@ def run_ours(args, world, rank, local):
                 "frac_of_burst_peak": round(achieved / peaks["bf16"], 4)}
     kernels = {"fmha_fwd": {"us": round(fwd_us, 2), "tflops": round(fwd_tf, 1)},
                "fmha_bwd": {"us": round(bwd_us, 2), "tflops": round(bwd_tf, 1)},
-               "pad": {"us": round(pad_us, 2), "GBps": round(pad_gbs, 1), "frac_hbm": round(pad_gbs / peaks["hbm"], 3)},
+               "pad": "fused into fmha_fwd's epilogue (ub_varlen_fmha_fwd_pad); standalone ub_pad under gather",
                "unpad_records": {"us": round(unpad_us, 2)}}
     fmha_only = mean_T * world / ((fwd_us + bwd_us) * 1e-6)
-    # main-stream timeline from the same events: idle gap before each step's forward (after
-    # the previous pad), forward end -> backward main kernel (= Delta prologue + gap), backward
-    # end -> pad start
+    # main-stream timeline from the same events: gap between a step's backward and the next
+    # step's forward, and forward end -> backward main kernel (= the Delta prologue + gaps)
     P = prof_events
-    F, Bk, Pd = kids[0], kids[1], kids[2]
+    F, Bk = kids[0], kids[1]
     timeline = {
-        "gap_before_fwd_us": round(float(np.mean([P[i - 1][Pd][1].elapsed_time(P[i][F][0]) for i in range(1, args.steps)])) * 1e3, 2),
+        "gap_bwd_end_to_next_fwd_us": round(float(np.mean([P[i - 1][Bk][1].elapsed_time(P[i][F][0]) for i in range(1, args.steps)])) * 1e3, 2),
         "fwd_end_to_bwd_main_us": round(float(np.mean([P[i][F][1].elapsed_time(P[i][Bk][0]) for i in range(args.steps)])) * 1e3, 2),
-        "bwd_end_to_pad_us": round(float(np.mean([P[i][Bk][1].elapsed_time(P[i][Pd][0]) for i in range(args.steps)])) * 1e3, 2)}
+        }
 
     e2e = None if args.no_e2e else run_e2e(args, wl, world)
     gather = gather_bench(wl, peaks) if rank == 0 else None
@@ -482,7 +481,7 @@ def run_ours(args, world, rank, local):
            "config": {"workload": f"bert_large_fmha_{args.dist}", "batch_per_gpu": B, "heads": H, "head_dim": D,
                       "max_seqlen": S, "p_dropout": args.p_dropout, "balance": args.balance, "skew": args.skew,
                       "parallelism": f"dp{world}", "fmha_ctas": wl.ctas, "l2": "rotating 3 input sets; per-step working set > L2",
-                      "step": "unpad records + exchange (side stream) | fmha fwd + bwd + pad (main stream)"},
+                      "step": "unpad records + exchange (side stream) | fmha fwd with fused pad + bwd (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
            "main_stream_timeline": timeline, "attn_dropout_0.1": drop01, "gather": gather,

@@ -134,6 +134,14 @@ size_t ub_fmha_workspace_bytes(const ub_fmha_params* prm, int is_bwd);
 ub_status ub_varlen_fmha_fwd(const ub_fmha_params* prm, const void* qkv, const int32_t* d_cu,
                              void* out, float* lse, void* ws, void* stream);
 
+/* Forward with the padding scatter fused in (a7 + a9): as ub_varlen_fmha_fwd, and the
+ * epilogue also writes O to padded [B, S, H, 64] bf16 at row b*S + i, with zeros in rows
+ * i >= L_b (the ub_pad result for a NULL pad row), from the same staged tiles -- the separate
+ * pad pass (a read of O and a write of the padded tensor) disappears.  S >= max_seqlen and
+ * S % 32 == 0 else UB_ERR_SHAPE; bf16 only (UB_ERR_UNSUPPORTED). */
+ub_status ub_varlen_fmha_fwd_pad(const ub_fmha_params* prm, const void* qkv, const int32_t* d_cu, void* out,
+                                 float* lse, void* padded, int32_t S, void* ws, void* stream);
+
 /* Backward: given dO, returns dQ, dK, dV (R4/R5 dropout replayed from the same key):
  *   Delta_i = sum_d dO_id O_id;  dV = P~^T dO;  dP = (dO V^T) * M/(1-p);
  *   dS = P * (dP - Delta);  dQ = scale dS K;  dK = scale dS^T Q. */

@@ -40,6 +40,7 @@ SIGNATURES = {
     "ub_pad": (i32, [vp, vp, vp, i32, i32, i64, i64, vp, vp]),
     "ub_fmha_workspace_bytes": (sz, [C.POINTER(FmhaParams), C.c_int]),
     "ub_varlen_fmha_fwd": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, vp]),
+    "ub_varlen_fmha_fwd_pad": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, i32, vp, vp]),
     "ub_varlen_fmha_bwd": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, vp, vp, vp]),
     "ub_dal_fwd": (i32, [vp, vp, vp, vp, i64, i32, f32, f32, u64, u64, vp, vp, vp, vp]),
     "ub_dal_bwd_workspace_bytes": (sz, [i64, i32]),

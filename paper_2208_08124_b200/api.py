@@ -108,8 +108,10 @@ def fmha_params(B, T, max_seqlen, heads, head_dim, dtype, scale=None, p_dropout=
 
 
 def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=None, p_dropout=0.0, seed=0,
-                    offset=0, out=None, lse=None, stream=None, num_ctas=0):
-    """Eq. (1) over packed qkv [T, 3, H, D]; returns (out [T,H,D], lse [H,T] fp32)."""
+                    offset=0, out=None, lse=None, stream=None, num_ctas=0, padded=None):
+    """Eq. (1) over packed qkv [T, 3, H, D]; returns (out [T,H,D], lse [H,T] fp32).
+    padded: optional [B, S, H, D] tensor that the forward also fills with O in the padded
+    layout, zeros past each length (a9 fused into the epilogue, ub_varlen_fmha_fwd_pad)."""
     T, three, H, D = qkv.shape
     assert three == 3
     B = cu.numel() - 1
@@ -119,8 +121,12 @@ def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=
     if lse is None:
         lse = torch.empty((H, T), dtype=torch.float32, device=qkv.device)
     ws = _workspace(lib().ub_fmha_workspace_bytes(C.byref(prm), 0), qkv.device, "fmha_fwd")
-    check(lib().ub_varlen_fmha_fwd(C.byref(prm), _ptr(qkv), _ptr(cu), _ptr(out), _ptr(lse), _ptr(ws),
-                                   _stream(stream)))
+    if padded is not None:
+        check(lib().ub_varlen_fmha_fwd_pad(C.byref(prm), _ptr(qkv), _ptr(cu), _ptr(out), _ptr(lse), _ptr(padded),
+                                           int(padded.shape[1]), _ptr(ws), _stream(stream)))
+    else:
+        check(lib().ub_varlen_fmha_fwd(C.byref(prm), _ptr(qkv), _ptr(cu), _ptr(out), _ptr(lse), _ptr(ws),
+                                       _stream(stream)))
     return out, lse
 
 

@@ -154,9 +154,23 @@ extern "C" ub_status ub_varlen_fmha_fwd(const ub_fmha_params* p, const void* qkv
     UB_REQUIRE(ws, UB_ERR_INVALID_ARG, "null workspace");
     UB_REQUIRE(((uintptr_t)qkv & 15) == 0 && ((uintptr_t)out & 15) == 0, UB_ERR_INVALID_ARG,
                "qkv/out must be 16-B aligned");
-    return fmha_fwd_sm100(*p, qkv, d_cu, out, lse, ws, as_stream(stream));
+    return fmha_fwd_sm100(*p, qkv, d_cu, out, lse, nullptr, 0, ws, as_stream(stream));
   }
   return fmha_fwd_simt(*p, static_cast<const float*>(qkv), d_cu, static_cast<float*>(out), lse, as_stream(stream));
+}
+
+extern "C" ub_status ub_varlen_fmha_fwd_pad(const ub_fmha_params* p, const void* qkv, const int32_t* d_cu,
+                                            void* out, float* lse, void* padded, int32_t S, void* ws, void* stream) {
+  clear_error();
+  ub_status st = check_fmha(p);
+  if (st != UB_OK) return st;
+  UB_REQUIRE(qkv && d_cu && out && lse && padded && ws, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(p->dtype == UB_BF16, UB_ERR_UNSUPPORTED, "the fused pad is on the bf16 path");
+  UB_REQUIRE(S >= p->max_seqlen && S % 32 == 0, UB_ERR_SHAPE, "S = %d: need S >= max_seqlen and S %% 32 == 0", S);
+  UB_REQUIRE((((uintptr_t)qkv | (uintptr_t)out | (uintptr_t)padded) & 15) == 0, UB_ERR_INVALID_ARG,
+             "qkv/out/padded must be 16-B aligned");
+  if ((st = require_sm100()) != UB_OK) return st;
+  return fmha_fwd_sm100(*p, qkv, d_cu, out, lse, padded, S, ws, as_stream(stream));
 }
 
 extern "C" ub_status ub_varlen_fmha_bwd(const ub_fmha_params* p, const void* qkv, const void* out,

@@ -69,6 +69,7 @@ struct Smem {
   uint8_t k[kStages][kTileBytes];
   uint8_t v[kStages][kTileBytes];
   uint8_t ostage[8][32 * 128];                    // per softmax warp: 32 output rows, SW128
+  uint8_t zeros[32 * 128];                        // a zero 32-row block: padded rows by TMA store
   uint64_t q_full[2], q_empty[2];
   uint64_t k_full[kStages], v_full[kStages], kv_empty[kStages];
   uint64_t s_full[2], s_free[2], p_full[2], o_done[2];   // per warpgroup
@@ -82,6 +83,8 @@ struct Params {
   FmhaPlanView plan;
   __nv_bfloat16* out;
   float* lse;
+  __nv_bfloat16* padded;   // fused a9: O also written to [B, S_pad, H, 64], zeros past L; NULL = off
+  int32_t S_pad;
   int32_t B, H, max_tiles;
   int64_t T;
   float scale, scale_log2;
@@ -102,7 +105,7 @@ __host__ __device__ constexpr uint32_t col_o(int x) { return 256u * x + 192u; }
 template <int kPoly, int kPack, bool kDropout, bool kBigB>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_constant__ CUtensorMap tmap_out,
-                const Params prm) {
+                const __grid_constant__ CUtensorMap tmap_pad, const Params prm) {
   // Taken straight from the __shared__ array so that every access compiles to LDS/STS (a
   // generic pointer would turn them into long-latency generic loads); the dynamic smem
   // window starts 1024-B aligned (checked), as the 128-B swizzle atoms require.
@@ -115,9 +118,14 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   (void)tr_n;
 
   pdl_launch_dependents();
+  if (warp == 10) {                                      // idle warps: the zero block for padded rows
+    for (uint32_t i = lane; i < sizeof(sm.zeros) / 16; i += 32) st_shared_v4(smem_u32(sm.zeros) + 16 * i, 0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
   if (warp == 8 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
     tma_prefetch_desc(&tmap_out);
+    if (prm.padded) tma_prefetch_desc(&tmap_pad);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sm.q_full[s], 1);
       mbar_init(&sm.q_empty[s], 1);
@@ -305,14 +313,34 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         __syncwarp();
         if (lane == 0) {
           tma_store_2d(&tmap_out, stage, pit.h * kD, pit.c0 + wrow0);
+          if (prm.padded) tma_store_2d(&tmap_pad, stage, pit.h * kD, pit.b * prm.S_pad + wrow0);
           bulk_commit_group();
         }
       } else if (row < pit.L) {
         uint4* op = reinterpret_cast<uint4*>(prm.out + ((int64_t)t_glob * H + pit.h) * kD);
 #pragma unroll
         for (int g = 0; g < 8; ++g) op[g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+        if (prm.padded) {
+          uint4* pp = reinterpret_cast<uint4*>(prm.padded + (((int64_t)pit.b * prm.S_pad + row) * H + pit.h) * kD);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) pp[g] = make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]);
+        }
       }
       if (row < pit.L) prm.lse[(int64_t)pit.h * prm.T + t_glob] = m_prev * prm.scale + logf(l_prev);
+      if (prm.padded && pit.tile + x == pit.nt - 1) {
+        // the sequence's last tile: zero its head's padded rows [L, S) -- lanes up to the
+        // tile end, then whole 32-row blocks from the zero tile, dealt over the 4 warps
+        if (row >= pit.L && row < prm.S_pad) {
+          uint4* pp = reinterpret_cast<uint4*>(prm.padded + (((int64_t)pit.b * prm.S_pad + row) * H + pit.h) * kD);
+#pragma unroll
+          for (int g = 0; g < 8; ++g) pp[g] = make_uint4(0, 0, 0, 0);
+        }
+        if (lane == 0) {
+          for (int32_t blk = pit.nt * (kTile / 32) + (int32_t)(warp & 3); blk * 32 < prm.S_pad; blk += 4)
+            tma_store_2d(&tmap_pad, sm.zeros, pit.h * kD, pit.b * prm.S_pad + blk * 32);
+          bulk_commit_group();
+        }
+      }
       TR(9);
     };
     // The two warpgroups take turns for their exp phases (named barriers 1 and 2 pass a token
@@ -498,18 +526,18 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
 }
 
 template <int P>
-static void (*pick_fwd(bool drop, bool big))(CUtensorMap, CUtensorMap, fwd::Params) {
+static void (*pick_fwd(bool drop, bool big))(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params) {
   if (big) return drop ? fwd::fmha_fwd_kernel<P, 0, true, true> : fwd::fmha_fwd_kernel<P, 0, false, true>;
   return drop ? fwd::fmha_fwd_kernel<P, 0, true, false> : fwd::fmha_fwd_kernel<P, 0, false, false>;
 }
 
 ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out, float* lse,
-                         void* ws, cudaStream_t s) {
+                         void* padded, int32_t S_pad, void* ws, cudaStream_t s) {
   // tuning knob: fraction (x/8) of exp2 pairs on the FMA pipe, 0 or 2 (measured default 2)
   // measured on config 2: 0 -> 64.5 us, 2 -> 58.4, 3 -> 62.2, 4 -> 68.4 (issue-bound beyond 2/8)
   static const int poly = env_int("UB_FWD_POLY", 2, 0, 4) >= 2 ? 2 : 0;
   const bool drop = p.p_dropout > 0.f, big = p.B > kPlanCap;
-  void (*kern)(CUtensorMap, CUtensorMap, fwd::Params) = poly == 2 ? pick_fwd<2>(drop, big) : pick_fwd<0>(drop, big);
+  void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params) = poly == 2 ? pick_fwd<2>(drop, big) : pick_fwd<0>(drop, big);
   {
     const ub_status sa = smem_attr_once(reinterpret_cast<const void*>(kern), (int)fwd::kSmemBytes);
     if (sa != UB_OK) return sa;
@@ -522,11 +550,17 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   if ((st = make_tmap_bf16(&tmap_out, out, (uint64_t)p.heads * fwd::kD, (uint64_t)p.T, (uint64_t)p.heads * fwd::kD * 2,
                            64, 32, 128)) != UB_OK)
     return st;
+  CUtensorMap tmap_pad = tmap_out;                       // (unused when padded is NULL)
+  if (padded && (st = make_tmap_bf16(&tmap_pad, padded, (uint64_t)p.heads * fwd::kD, (uint64_t)p.B * S_pad,
+                                     (uint64_t)p.heads * fwd::kD * 2, 64, 32, 128)) != UB_OK)
+    return st;
   FmhaPlanView v = fmha_plan_view(ws, p.B);
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
   if (p.B > kPlanCap && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 2, v, s)) != UB_OK) return st;
 
   fwd::Params prm{};
+  prm.padded = static_cast<__nv_bfloat16*>(padded);
+  prm.S_pad = S_pad;
   prm.cu = d_cu;
   prm.plan = v;
   prm.out = static_cast<__nv_bfloat16*>(out);
@@ -550,7 +584,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfFwd, 0, s);
-  launch_pdl(kern, dim3(grid), dim3(fwd::kThreads), fwd::kSmemBytes, s, tmap, tmap_out, prm);
+  launch_pdl(kern, dim3(grid), dim3(fwd::kThreads), fwd::kSmemBytes, s, tmap, tmap_out, tmap_pad, prm);
   UB_CHECK_LAUNCH();
   prof_record(kProfFwd, 1, s);
   return UB_OK;

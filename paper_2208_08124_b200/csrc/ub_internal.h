@@ -61,8 +61,8 @@ FmhaPlanView fmha_plan_view(void* ws, int32_t B);
 ub_status launch_fmha_plan(const int32_t* d_cu, int32_t B, int32_t H, int32_t max_tiles, int32_t tiles_per_item,
                            FmhaPlanView v, cudaStream_t s);
 
-ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out,
-                         float* lse, void* ws, cudaStream_t s);
+ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out, float* lse,
+                         void* padded, int32_t S_pad, void* ws, cudaStream_t s);
 ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* out, const float* lse,
                          const void* dout, const int32_t* d_cu, void* dqkv, void* ws, cudaStream_t s);
 size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p);

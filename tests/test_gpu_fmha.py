@@ -172,3 +172,22 @@ def test_bf16_more_sequences_than_smem_plan(ub):
         assert_close(o[s:e].float().numpy(), O, f"O seq{b}")
         for i, name in enumerate("qkv"):
             assert_close(d[s:e, i].float().numpy(), dq[:, i], f"d{name} seq{b}")
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_fwd_with_fused_pad(ub, p):
+    """ub_varlen_fmha_fwd_pad (a7 + a9): out / lse identical to the plain forward, padded
+    identical (bitwise) to ub_pad of out -- zeros past each length, including whole padded
+    tiles and sequences of one token."""
+    L = np.array([1, 31, 32, 33, 127, 128, 129, 300, 512, 64], np.int32)
+    lengths, off, qkv, dout = make_batch(L, 4, 64)
+    qd = qkv.cuda()
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    S = 512
+    o1, l1 = ub.varlen_fmha_fwd(qd, cu, S, None, p, 3, 0)
+    padded = torch.full((len(L), S, 4, 64), float("nan"), dtype=torch.bfloat16, device="cuda")
+    o2, l2 = ub.varlen_fmha_fwd(qd, cu, S, None, p, 3, 0, padded=padded)
+    ref = ub.pad(o1, cu, len(L), S)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    assert torch.equal(padded.view(torch.int16), ref.view(torch.int16))
