@@ -481,6 +481,7 @@ def run_ours(args, world, rank, local):
     e2e = None if args.no_e2e else run_e2e(args, wl, world)
     gather = gather_bench(wl, peaks) if rank == 0 else None
     encoder = encoder_bench(wl, peaks) if rank == 0 and not args.no_encoder else None
+    embedding = embedding_bench(wl, peaks) if rank == 0 and not args.no_encoder else None
     drop01 = dropout_bench(wl) if rank == 0 and args.p_dropout == 0.0 else None
     out = {"metric": "unpadded FMHA fwd+bwd tokens/s (BERT-large)", "value": round(value, 1), "unit": "tokens/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
@@ -493,7 +494,7 @@ def run_ours(args, world, rank, local):
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
            "main_stream_timeline": timeline, "attn_dropout_0.1": drop01, "gather": gather,
-           "encoder_attn_sublayer": encoder, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
+           "encoder_attn_sublayer": encoder, "embedding": embedding, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
            "host_us_per_step": dict(zip(["step_setup", "fwd_call", "bwd_call", "pad_call", "unpad_call", "finish_call",
                                               "begin_call"],
                                         [round(1e6 * float(x), 1) for x in np.median(np.array(marks), axis=0)]),
@@ -586,6 +587,49 @@ def dropout_bench(wl, iters=10):
         res[name + "_us"] = round(float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3, 2)
     res["fmha_only_tokens_per_s"] = round(T / ((res["fwd_us"] + res["bwd_us"]) * 1e-6), 1)
     res["note"] = "main kernels only, L2-warm single batch; headline runs p = 0 (config 2 names no dropout)"
+    return res
+
+
+def embedding_bench(wl, peaks, iters=10):
+    """NEXT-4: unpadded BERT embedding fwd / bwd (fp32 gradients, 16-B vector reductions) on
+    the config-2 packed batch, vocab 30 522, Zipf-like ids.  Algorithmic bytes: fwd the output
+    plus each distinct table row once; bwd 1 row read + 2 fp32 row updates per token (word,
+    position; the token-type rows are reduced per CTA)."""
+    ub = wl.ub
+    st = wl.sets[0]
+    T, cu = st["T"], st["cu_local"]
+    E, Vv, P = H * D, 30522, S        # noqa: N806
+    rng = np.random.default_rng(0)
+    off = cu.cpu().numpy().astype(np.int64)
+    ids = torch.from_numpy(np.minimum(rng.zipf(1.2, T) - 1, Vv - 1).astype(np.int32)).to(wl.dev)
+    pos = torch.from_numpy((np.arange(T) - np.repeat(off[:-1], np.diff(off))).astype(np.int32)).to(wl.dev)
+    seg = torch.from_numpy((rng.random(T) < 0.5).astype(np.int32)).to(wl.dev)
+    ww = (0.02 * torch.randn((Vv, E), device=wl.dev)).to(torch.bfloat16)
+    wp = (0.02 * torch.randn((P, E), device=wl.dev)).to(torch.bfloat16)
+    wt = (0.02 * torch.randn((2, E), device=wl.dev)).to(torch.bfloat16)
+    dout = torch.randn((T, E), device=wl.dev).to(torch.bfloat16)
+    out = torch.empty((T, E), dtype=torch.bfloat16, device=wl.dev)
+    dws = [torch.zeros((n, E), dtype=torch.float32, device=wl.dev) for n in (Vv, P, 2)]
+    res = {}
+    uniq = int(torch.unique(ids).numel())
+    # fwd compulsory HBM bytes: the output plus each distinct table row once (hot rows of the
+    # Zipf ids, the position and type tables stay in L2)
+    for name, fn, nb in (("fwd", lambda: ub.embedding_fwd(ids, pos, seg, ww, wp, wt, out=out),
+                          (T + uniq + P + 2) * E * 2),
+                         ("bwd", lambda: ub.embedding_bwd(dout, ids, pos, seg, *dws), T * E * 2 + 2 * T * E * 4)):
+        fn()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(2_000_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / iters * 1e3
+        res[name] = {"us": round(us, 2), "GBps": round(nb / (us * 1e-6) / 1e9, 1),
+                     "frac_hbm": round(nb / (us * 1e-6) / 1e9 / peaks["hbm"], 3)}
+    res["config"] = f"T={T}, E={E}, vocab {Vv}, Zipf(1.2) ids, fp32 gradients"
     return res
 
 

@@ -170,6 +170,25 @@ ub_status ub_dal_bwd(const void* dy, const void* a, const void* res, const void*
                      void* da, void* dres, float* dgamma, float* dbeta, void* ws, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * Unpadded BERT embedding (P:525-535 embedding backward with packed atomics;
+ * SURVEY §8(f) NEXT-4), on packed tokens (reading R23):
+ *   ub_embedding_fwd: out[t] = W_word[ids[t]] + W_pos[pos[t]] + W_type[seg[t]]  (bf16 [T, E])
+ *   ub_embedding_bwd: dW_word[ids[t]] += dout[t], dW_pos[pos[t]] += dout[t],
+ *                     dW_type[seg[t]] += dout[t]  -- ACCUMULATES into the caller's dW
+ *                     (zero them first); grad_dtype UB_FP32 (16-B fp32 vector reductions)
+ *                     or UB_BF16 (bf16x2 vector reductions, the paper's packed-atomic form,
+ *                     P:535; less precise for frequent tokens).  Summation order is not
+ *                     fixed (atomics): results agree with the oracle within rounding.
+ * ids / pos / seg: int32 [T] device, values in range (not validated on the device, like
+ * cu_seqlens); tables bf16 [rows, E]; E a multiple of 8 in [8, 2048] else UB_ERR_UNSUPPORTED;
+ * n_type (token-type rows) in [1, 2]; 16-B aligned arrays.  Async on stream. */
+ub_status ub_embedding_fwd(const int32_t* ids, const int32_t* pos, const int32_t* seg, const void* w_word,
+                           const void* w_pos, const void* w_type, int64_t T, int32_t E, void* out, void* stream);
+ub_status ub_embedding_bwd(const void* dout, const int32_t* ids, const int32_t* pos, const int32_t* seg, int64_t T,
+                           int32_t E, int32_t n_type, int32_t grad_dtype, void* dw_word, void* dw_pos, void* dw_type,
+                           void* stream);
+
+/* ------------------------------------------------------------------------------------
  * Linear layers (P:410 Linear fusion through cuBLASLt; P:416 residual gradient through the
  * GEMM's beta), row-major packed rows, bf16 activations / weights, fp32 accumulation:
  *   ub_linear_fwd: y[T,N] = x[T,K] W[N,K]^T + b[N]    (b may be NULL; bias in the epilogue)

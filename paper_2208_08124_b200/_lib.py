@@ -45,6 +45,8 @@ SIGNATURES = {
     "ub_dal_fwd": (i32, [vp, vp, vp, vp, i64, i32, f32, f32, u64, u64, vp, vp, vp, vp]),
     "ub_dal_bwd_workspace_bytes": (sz, [i64, i32]),
     "ub_dal_bwd": (i32, [vp, vp, vp, vp, vp, vp, i64, i32, f32, u64, u64, vp, vp, vp, vp, vp, vp]),
+    "ub_embedding_fwd": (i32, [vp, vp, vp, vp, vp, vp, i64, i32, vp, vp]),
+    "ub_embedding_bwd": (i32, [vp, vp, vp, vp, i64, i32, i32, i32, vp, vp, vp, vp]),
     "ub_linear_workspace_bytes": (sz, []),
     "ub_linear_fwd": (i32, [vp, vp, vp, i64, i32, i32, vp, vp, vp]),
     "ub_linear_bwd": (i32, [vp, vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp]),

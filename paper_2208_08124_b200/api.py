@@ -172,6 +172,25 @@ def dal_bwd(dy: torch.Tensor, a: torch.Tensor, res: torch.Tensor, gamma: torch.T
     return da, dres, dgamma, dbeta
 
 
+# ------------------------------------------------------------------ embedding (NEXT-4)
+def embedding_fwd(ids, pos, seg, w_word, w_pos, w_type, out=None, stream=None):
+    """out[t] = W_word[ids[t]] + W_pos[pos[t]] + W_type[seg[t]] on packed tokens."""
+    T, E = ids.numel(), w_word.shape[1]
+    out = out if out is not None else torch.empty((T, E), dtype=w_word.dtype, device=w_word.device)
+    check(lib().ub_embedding_fwd(_ptr(ids), _ptr(pos), _ptr(seg), _ptr(w_word), _ptr(w_pos), _ptr(w_type), int(T),
+                                 int(E), _ptr(out), _stream(stream)))
+    return out
+
+
+def embedding_bwd(dout, ids, pos, seg, dw_word, dw_pos, dw_type, stream=None):
+    """Accumulate dout rows into the (zeroed) fp32 or bf16 table gradients."""
+    T, E = dout.shape
+    gd = UB_FP32 if dw_word.dtype == torch.float32 else UB_BF16
+    check(lib().ub_embedding_bwd(_ptr(dout), _ptr(ids), _ptr(pos), _ptr(seg), int(T), int(E), int(dw_type.shape[0]),
+                                 gd, _ptr(dw_word), _ptr(dw_pos), _ptr(dw_type), _stream(stream)))
+    return dw_word, dw_pos, dw_type
+
+
 # ------------------------------------------------------------------ Linear (cuBLASLt) and the encoder sub-layer
 def linear_fwd(x: torch.Tensor, W: torch.Tensor, b: torch.Tensor | None = None, out=None, stream=None):
     """y[T, N] = x[T, K] W[N, K]^T + b (P:410)."""
