@@ -58,14 +58,6 @@ constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
 constexpr uint32_t kPBytes = kTile * kTile * 2;   // 32 KB
 constexpr int kThreads = 512;
 constexpr uint32_t kQStages = 3;                  // Q / dO / LSE / Delta pipeline depth
-#ifndef UB_BWD_DQ_DIRECT
-#define UB_BWD_DQ_DIRECT 0
-#endif
-// UB_BWD_DQ_DIRECT = 1: the dQ partials of passes before the last go straight from registers
-// to the fp32 scratch (st.global / red.global.add.v4, each lane its own 256-B row) instead of
-// smem staging + TMA store / reduce.  Measured slower (139 vs 113 us on config 2: the L2
-// atomics of 4-KB-per-warp partials are far less efficient than bulk reduces); kept for A/B.
-constexpr bool kDqDirect = UB_BWD_DQ_DIRECT != 0;
 constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDQ = 320, kColDV = 384, kColDK = 448;
 
 struct Smem {
@@ -259,12 +251,10 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         umma_commit(&sm.qdo_empty[p_st]);              // Q_i / dO_i no longer needed
         mbar_wait(&sm.dq_empty, (g_cnt & 1) ^ 1);      // the epilogue has read dQ of the previous pair
         tc_fence_after();
-#ifndef UB_BWD_EXPERIMENT_NO_DQ_MMA
 #pragma unroll
         for (uint32_t k = 0; k < kTile / 16; ++k)        // dQ = dS K, K = key rows, 16 per MMA
           umma_bf16_ss(tmem + kColDQ, sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024),
                        sdesc_sw128(p_kaddr + k * 2048, 8192, 1024), kIdescQ, k > 0);
-#endif
         umma_commit(&sm.dq_full);                      // grads done: P~^T / dS free, dQ_i in TMEM
         TR(19);
         ++g_cnt;
@@ -283,9 +273,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           TR(17);
           for (int32_t i = 0; i < it.nt; ++i, ++qit) {
             const uint32_t st = qit % kQStages;
-#ifndef UB_BWD_EXPERIMENT_NO_QDO_WAIT
             mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);
-#endif
             TR(18);
             mbar_wait(&sm.s_free, (s_cnt & 1) ^ 1);
             TR(10);
@@ -386,23 +374,15 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           }
           // grads of the previous pair done => P~^T TMEM and the dS smem tile are free
           TR(4);
-#ifndef UB_BWD_EXPERIMENT_NO_GRAD_WAIT
           mbar_wait(&sm.dq_full, (g_cnt & 1) ^ 1);
-#endif
           TR(5);
           tc_fence_after();
           tmem_st32(t_row + kColP + x * 32, pp);
-#ifndef UB_BWD_EXPERIMENT_NO_DS_STS
 #pragma unroll
           for (int g = 0; g < 8; ++g)
             st_shared_v4(ds_addr + sw128_off(r, g), pd[4 * g], pd[4 * g + 1], pd[4 * g + 2], pd[4 * g + 3]);
-#else
-          if (pd[0] == 0x7fc07fc0u && pd[31] == 0x7fc07fc0u) st_shared_v4(ds_addr, pd[1], pd[2], pd[3], pd[4]);
-#endif
           tmem_st_wait();
-#ifndef UB_BWD_EXPERIMENT_NO_DS_FENCE
           fence_proxy_async_smem();
-#endif
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.pds_full);
@@ -447,7 +427,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           // this pass's op on tile i follows the previous pass's one (async TMA ops of this
           // warp complete in any order: wait for that group); the last pass re-reads the
           // partial, which is warmed into L1 before dQ is even ready
-          if (!first && full && !kDqDirect) {
+          if (!first && full) {
             if (lane == 0) {
               bulk_wait_group_n((int)(ng - gq[i]));
               if (last) fence_proxy_async_global();
@@ -547,7 +527,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             // pass 0 stores the fp32 partial, middle passes add to it
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
-              if (full && !kDqDirect) {
+              if (full) {
                 stage_free();
 #pragma unroll
                 for (int g = 0; g < 8; ++g)
@@ -556,13 +536,8 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-#if defined(UB_BWD_EXPERIMENT_NO_DQ_OUT)   // timing experiments only (wrong dQ)
-#elif defined(UB_BWD_EXPERIMENT_DQ_STORE_ONLY)
-                  tma_store_2d(&tmap_dq, stage, half * 32, arow0);
-#else
                   if (first) tma_store_2d(&tmap_dq, stage, half * 32, arow0);
                   else tma_reduce_add_2d(&tmap_dq, stage, half * 32, arow0);
-#endif
                   bulk_commit_group();
                   ++ng;
                 }

@@ -18,8 +18,7 @@
 //               item's first), so the softmax never waits for an item boundary
 //   warps 10-11 idle (the third warpgroup is whole so that setmaxnreg can move registers
 //               from it to the softmax warpgroups: 208 vs 88 per thread)
-// Optionally (UB_FWD_EXP_TURNS) the softmax warpgroups take turns for their exp phases
-// (named-barrier token; measured neutral, off by default).  Each warpgroup defers its epilogue (O / l -> bf16 -> TMA store, LSE) into the first key tile of its
+// Each softmax warpgroup defers its epilogue (O / l -> bf16 -> TMA store, LSE) into the first key tile of its
 // next item, after that tile's P has been handed to the MMA.
 // TMEM (512 columns): per warpgroup x: S at 256x (128 cols fp32), P at 256x+128 (64 cols,
 // bf16 pairs), O at 256x+192 (64 cols fp32).
@@ -38,10 +37,6 @@
 namespace ub {
 namespace fwd {
 
-#ifndef UB_FWD_SETMAXNREG
-#define UB_FWD_SETMAXNREG 1
-#endif
-
 #ifdef UB_TRACE
 // Debug timeline (trace builds only): CTA 0, lane 0 of every warp records (event, clock64).
 __device__ uint64_t g_trace[10 * 1024];
@@ -57,12 +52,8 @@ __device__ uint64_t g_trace[10 * 1024];
 constexpr int kD = 64;
 constexpr int kStages = 3;
 constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
-constexpr int kThreads = UB_FWD_SETMAXNREG ? 384 : 320;   // 3 warpgroups (setmaxnreg is per warpgroup)
+constexpr int kThreads = 384;                     // 3 warpgroups (setmaxnreg is per warpgroup)
 constexpr float kRescaleThreshold = 8.0f;         // log2 units
-#ifndef UB_FWD_EXP_TURNS
-#define UB_FWD_EXP_TURNS 0   // measured neutral on config 2 (60.4-61.3 us either way); kept for A/B
-#endif
-constexpr bool kExpTurns = UB_FWD_EXP_TURNS != 0;
 
 struct Smem {
   uint8_t q[2][2][kTileBytes];                    // [item slot][warpgroup]
@@ -155,7 +146,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
 
   if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
-    if (UB_FWD_SETMAXNREG) regs_dec<88>();
+    regs_dec<88>();
     if (lane == 0) {
       uint32_t items = 0, kv_it = 0;
       WorkItem it;
@@ -180,7 +171,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
-    if (UB_FWD_SETMAXNREG) regs_dec<88>();
+    regs_dec<88>();
     if (lane == 0) {
       // One stream of key tiles across items: the S of the next tile -- the next item's first
       // tile at an item's last -- is issued before the PV of the current one, so a softmax
@@ -266,7 +257,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ softmax warpgroups
-    if (UB_FWD_SETMAXNREG) regs_inc<208>();
+    regs_inc<208>();
     const int x = (int)(warp >> 2);                       // warpgroup / query tile of the pair
     const uint32_t r = threadIdx.x - 128u * x;            // row inside the tile
     const uint32_t t_row = tmem + (((warp & 3) * 32) << 16);
@@ -343,21 +334,9 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       }
       TR(9);
     };
-    // The two warpgroups take turns for their exp phases (named barriers 1 and 2 pass a token
-    // A0 B0 A1 B1 ...): each exp phase has the MUFU of its SMSPs to itself, and the other
-    // warpgroup's TMEM loads, stores and waits hide under it.  Warpgroup B passes the token
-    // through the key tiles of single-tile items it sits out.
-    if (kExpTurns && x == 1) named_bar_arrive(1, 256);
     WorkItem it;
     for (int32_t ri = 0; decode_item_smem<kBigB>(snake_item(ri, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); ++ri) {
-      if (x >= it.ntile) {
-        if (kExpTurns)
-          for (int32_t j = 0; j < it.nt; ++j) {
-            named_bar_sync(2, 256);
-            named_bar_arrive(1, 256);
-          }
-        continue;
-      }
+      if (x >= it.ntile) continue;
       const int32_t row = (it.tile + x) * kTile + (int32_t)r;
       const uint32_t t_glob = (uint32_t)(it.c0 + row);
       float m_run = -INFINITY, l = 0.f;
@@ -408,7 +387,6 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         uint64_t acc2[4] = {0, 0, 0, 0};
         uint32_t pk[kTile / 2];
         uint32_t bits16 = 0;
-        if (kExpTurns) named_bar_sync(1 + x, 256);     // my turn for the exp phase
 #pragma unroll
         for (int g = 0; g < kTile / 8; ++g) {          // 8 keys at a time: exp2, sum, dropout, pack
           float e8[8];
@@ -444,7 +422,6 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           f2unpack(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])), a0, a1);
           rs = a0 + a1;
         }
-        if (kExpTurns) named_bar_arrive(2 - x, 256);   // the other warpgroup's turn
 
         TR(4);
         const bool defer = j == 0 && have_prev;
@@ -491,7 +468,6 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       m_prev = m_run;
       pit = it;
     }
-    if (kExpTurns && x == 0) named_bar_sync(1, 256);    // B's last token
     if (have_prev) {
       TR(7);
       uint32_t opk[32];
@@ -499,7 +475,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       epilogue(opk);
     }
   } else {
-    if (UB_FWD_SETMAXNREG) regs_dec<88>();                // warps 10-11: idle
+    regs_dec<88>();                // warps 10-11: idle
   }
 
   if (warp < 8 && lane == 0) bulk_wait_group0();        // output stores complete before exit
