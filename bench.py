@@ -90,6 +90,26 @@ def load_traffic():
         return json.load(f).get("dram_bytes_per_launch", {})
 
 
+def load_tensor_pipe():
+    """ncu sm__pipe_tensor_cycles_active (% of peak, active cycles) per FMHA kernel from the
+    newest round in the committed summary -- the TC-utilisation evidence BASELINE names."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        rounds = json.load(f).get("rounds", {})
+    if not rounds:
+        return {}
+    tag = sorted(rounds)[-1]
+    key = "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"
+    out = {"round": tag}
+    for k in ("fmha_fwd", "fmha_bwd"):
+        v = rounds[tag].get(k, {}).get(key)
+        if v:
+            out[k] = float(v["value"])
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -469,6 +489,15 @@ def run_ours(args, world, rank, local):
                "pad": "fused into fmha_fwd's epilogue (ub_varlen_fmha_fwd_pad); standalone ub_pad under gather",
                "unpad_records": {"us": round(unpad_us, 2)}}
     fmha_only = mean_T * world / ((fwd_us + bwd_us) * 1e-6)
+    # TC utilisation (BASELINE metric), three ways: FA convention 14 H D sum L^2
+    # per fwd+bwd (recompute credited), strict 12 H D sum L^2, and ncu's tensor-pipe activity
+    s2 = float(np.mean([float((np.asarray(lens_used[i], np.int64) ** 2).sum()) for i in prof_steps]))
+    fb_s = (fwd_us + bwd_us) * 1e-6
+    tc_util = {"fa_convention_tflops": round(14 * H * D * s2 / fb_s / 1e12, 1),
+               "strict_tflops": round(12 * H * D * s2 / fb_s / 1e12, 1),
+               "fa_frac_of_burst_peak": round(14 * H * D * s2 / fb_s / 1e12 / peaks["bf16"], 4),
+               "ncu_tensor_pipe_active_pct": load_tensor_pipe(),
+               "note": "fwd (incl. its fused pad writes) + bwd main kernels, in-step device time"}
     # main-stream timeline from the same events: gap between a step's backward and the next
     # step's forward, and forward end -> backward main kernel (= the Delta prologue + gaps)
     P = prof_events
@@ -492,6 +521,7 @@ def run_ours(args, world, rank, local):
                       "parallelism": f"dp{world}", "fmha_ctas": wl.ctas, "l2": "rotating 3 input sets; per-step working set > L2",
                       "step": "unpad records + exchange (side stream) | fmha fwd with fused pad + bwd (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
+           "tc_util": tc_util,
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
            "main_stream_timeline": timeline, "attn_dropout_0.1": drop01, "gather": gather,
            "encoder_attn_sublayer": encoder, "embedding": embedding, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
