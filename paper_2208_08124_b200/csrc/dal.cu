@@ -254,7 +254,8 @@ static void launch_bwd(bool drop, int grid, cudaStream_t s, const void* dy, cons
                        const Params& q) {
   auto k = drop ? dal_bwd_kernel<NV, true> : dal_bwd_kernel<NV, false>;
   const int smem = kWarps * 2 * q.E * (int)sizeof(float);
-  smem_attr_once(reinterpret_cast<const void*>(k), smem);
+  // the attribute is set once per kernel: the largest E the kernel supports
+  smem_attr_once(reinterpret_cast<const void*>(k), kWarps * 2 * (32 * kMaxVec * 8) * (int)sizeof(float));
   k<<<grid, kThreads, smem, s>>>(static_cast<const uint4*>(dy), static_cast<const uint4*>(a),
                               static_cast<const uint4*>(res), static_cast<const uint4*>(gamma), mean, rstd,
                               static_cast<uint4*>(da), static_cast<uint4*>(dres), part, q);

@@ -193,7 +193,8 @@ extern "C" ub_status ub_embedding_bwd(const void* dout, const int32_t* ids, cons
   auto k = f32 ? (nv <= 4 ? emb::embedding_bwd_kernel<4, true> : emb::embedding_bwd_kernel<8, true>)
                : (nv <= 4 ? emb::embedding_bwd_kernel<4, false> : emb::embedding_bwd_kernel<8, false>);
   const int smem = emb::kWarps * 2 * E * (int)sizeof(float);
-  smem_attr_once(reinterpret_cast<const void*>(k), smem);
+  // the attribute is set once per kernel: the largest E the kernel supports
+  smem_attr_once(reinterpret_cast<const void*>(k), emb::kWarps * 2 * (32 * emb::kMaxVec * 8) * (int)sizeof(float));
   launch_pdl(k, dim3(emb::grid_for(T)), dim3(emb::kThreads), (size_t)smem, as_stream(stream),
              static_cast<const uint4*>(dout), ids, pos, seg, dw_word, dw_pos, dw_type, T, (int32_t)V, n_type);
   UB_CHECK_LAUNCH();

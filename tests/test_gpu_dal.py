@@ -76,6 +76,19 @@ def test_dal_bert_large_full_size_sampled(ub):
     assert_close(db.cpu().numpy(), DB, "dbeta", max_abs=1.0)
 
 
+def test_dal_bwd_growing_width(ub):
+    """Backward calls with E growing across calls (the shared-memory attribute is set once
+    per kernel for its largest width)."""
+    for E in (64, 1024, 2048):
+        a, res, gamma, beta, dy = _inputs(16, E, E)
+        y, mean, rstd = ub.dal_fwd(a.cuda(), res.cuda(), gamma.cuda(), beta.cuda())
+        da, dres, dg, db = ub.dal_bwd(dy.cuda(), a.cuda(), res.cuda(), gamma.cuda(), mean, rstd)
+        torch.cuda.synchronize()
+        f64 = lambda t: t.double().numpy()
+        DA, DRES, DG, DB = odal.dal_bwd(f64(dy), f64(a), f64(res), f64(gamma))
+        assert_close(dres.float().cpu().numpy(), DRES, f"dres E={E}")
+
+
 def test_dal_invalid_arguments(ub):
     from paper_2208_08124_b200 import UbError
     a = torch.zeros((4, 12), dtype=torch.bfloat16, device="cuda")
