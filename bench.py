@@ -512,6 +512,7 @@ def run_ours(args, world, rank, local):
     encoder = encoder_bench(wl, peaks) if rank == 0 and not args.no_encoder else None
     embedding = embedding_bench(wl, peaks) if rank == 0 and not args.no_encoder else None
     drop01 = dropout_bench(wl) if rank == 0 and args.p_dropout == 0.0 else None
+    sweep = dist_sweep(wl, peaks) if rank == 0 and not args.no_encoder else None
     out = {"metric": "unpadded FMHA fwd+bwd tokens/s (BERT-large)", "value": round(value, 1), "unit": "tokens/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
@@ -523,7 +524,7 @@ def run_ours(args, world, rank, local):
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
            "tc_util": tc_util,
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
-           "main_stream_timeline": timeline, "attn_dropout_0.1": drop01, "gather": gather,
+           "main_stream_timeline": timeline, "attn_dropout_0.1": drop01, "length_sweep": sweep, "gather": gather,
            "encoder_attn_sublayer": encoder, "embedding": embedding, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
            "host_us_per_step": dict(zip(["step_setup", "fwd_call", "bwd_call", "pad_call", "unpad_call", "finish_call",
                                               "begin_call"],
@@ -661,6 +662,45 @@ def embedding_bench(wl, peaks, iters=10):
                      "frac_hbm": round(nb / (us * 1e-6) / 1e9 / peaks["hbm"], 3)}
     res["config"] = f"T={T}, E={E}, vocab {Vv}, Zipf(1.2) ids, fp32 gradients"
     return res
+
+
+def dist_sweep(wl, peaks, iters=10):
+    """BASELINE config 5 on one GPU: the FMHA fwd + bwd main kernels on 56-sequence batches of
+    each length distribution (uniform, MLPerf-like, bimodal 64/512), device time from the
+    library's events, with the fwd+bwd TC utilisation (FA convention, burst peak)."""
+    from paper_2208_08124_b200 import api
+    ub = wl.ub
+    out = {}
+    for dist in ("uniform", "mlperf_like_v0", "bimodal"):
+        L = synth.gen_lengths(dist, B, 0).astype(np.int64)
+        T = int(L.sum())
+        off = np.concatenate([[0], np.cumsum(L)]).astype(np.int32)
+        cu = torch.from_numpy(off).to(wl.dev)
+        qkv = synth.gen_normal_device((T, 3, H, D), 11, wl.dev)
+        dout = synth.gen_normal_device((T, H, D), 12, wl.dev)
+        o, lse = ub.varlen_fmha_fwd(qkv, cu, S)
+        res = {}
+        for name, kid, fn in (("fwd", api.PROF_FWD, lambda: ub.varlen_fmha_fwd(qkv, cu, S, out=o, lse=lse)),
+                              ("bwd", api.PROF_BWD, lambda: ub.varlen_fmha_bwd(qkv, o, lse, dout, cu, S))):
+            fn()
+            torch.cuda.synchronize()
+            torch.cuda._sleep(2_000_000)
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+            for k in range(iters):
+                api.profile_events(kid, *ev[k])
+                fn()
+            api.profile_events(kid)
+            torch.cuda.synchronize()
+            res[name + "_us"] = round(float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3, 2)
+        s2 = float((L ** 2).sum())
+        fb = (res["fwd_us"] + res["bwd_us"]) * 1e-6
+        res["tokens_per_s"] = round(T / fb, 1)
+        res["fa_convention_tflops"] = round(14 * H * D * s2 / fb / 1e12, 1)
+        res["fa_frac_of_burst_peak"] = round(14 * H * D * s2 / fb / 1e12 / peaks["bf16"], 4)
+        res["T"] = T
+        out[dist] = res
+    out["note"] = "main kernels only, one L2-warm batch each (seed 0), p = 0"
+    return out
 
 
 def encoder_bench(wl, peaks, iters=10):
