@@ -237,7 +237,7 @@ __device__ __forceinline__ uint64_t ex2_poly2(float xa, float xb) {
   const uint64_t x2 = f2pack(xa, xb);
   const uint64_t t2 = fadd2(x2, f2pack(magic, magic));
   const uint64_t n2 = fadd2(t2, f2pack(-magic, -magic));
-  const uint64_t f2 = fadd2(x2, n2 ^ 0x8000000080000000ull);       // x - n
+  const uint64_t f2 = ffma2(n2, f2pack(-1.f, -1.f), x2);          // x - n (exact; one op)
   uint64_t p2 = ffma2(f2, f2pack(0.05500874f, 0.05500874f), f2pack(0.24221049f, 0.24221049f));
   p2 = ffma2(p2, f2, f2pack(0.69328298f, 0.69328298f));
   p2 = ffma2(p2, f2, f2pack(1.0f, 1.0f));
