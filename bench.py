@@ -32,6 +32,16 @@ import sys
 import tempfile
 import time
 
+
+def _claim_stdout():
+    """stdout carries exactly one JSON line: keep a private handle on it and point fd 1 at
+    stderr, so that library banners written straight to fd 1 (NCCL prints its version there
+    at communicator init) cannot land on it."""
+    sys.stdout.flush()
+    out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    return out
+
 import numpy as np
 import torch
 
@@ -882,19 +892,20 @@ def run_e2e(args, wl, world):
 
 def main():
     args = parse()
+    json_out = _claim_stdout()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
         out = run_reference(args, world, rank)
         if out is not None:
-            print(json.dumps(out), flush=True)
+            print(json.dumps(out), file=json_out, flush=True)
         return
     world, rank, local = dist_init(args.gpus)
     out, wl = run_ours(args, world, rank, local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=json_out, flush=True)
     wl.comm.close()
     if world > 1:
         import torch.distributed as dist
