@@ -75,8 +75,10 @@ struct Smem {
   uint64_t s_full, s_free, pds_full, dq_full, dq_empty, dkv_full, dkv_free;
   uint32_t tmem_base;
   PlanSmem plan;
+  ItemTable items;                  // this CTA's items, decoded once
 };
 constexpr size_t kSmemBytes = sizeof(Smem);
+static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 
 struct Params {
   const int32_t* cu;
@@ -153,7 +155,11 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   }
   if (warp == 13) tmem_alloc(&sm.tmem_base, 512);
   pdl_wait();                                            // everything below may read / write global memory
-  if (!kBigB && warp == 12) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 0, lane);
+  if (!kBigB && warp == 12) {
+    build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 0, lane);
+    __syncwarp();
+    build_item_table(sm.items, sm.plan, prm.cu, prm.B, prm.H, 0, (int32_t)blockIdx.x, (int32_t)gridDim.x, lane);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -161,7 +167,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   const int32_t H = prm.H;
   const int32_t G = (int32_t)gridDim.x, cta = (int32_t)blockIdx.x;
 #define UB_ITEMS(r, it) \
-  for (int32_t r = 0; decode_item_smem<kBigB>(snake_item(r, cta, G), sm.plan, prm.plan, prm.cu, prm.B, H, 0, it); ++r)
+  for (int32_t r = 0; next_item<kBigB>(r, sm.items, prm.plan, prm.cu, prm.B, H, 0, cta, G, it); ++r)
   // each role re-sizes its registers at its entry, inside its branch (ptxas takes the
   // minimum where paths merge); setmaxnreg is warpgroup-uniform
 
@@ -613,8 +619,15 @@ size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p) {
 
 ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* out, const float* lse, const void* dout,
                          const int32_t* d_cu, void* dqkv, void* ws, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t max_items = (int64_t)p.heads * p.B;
+  const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
+  const int grid = (int)std::min<int64_t>(ctas, max_items);
   const bool drop = p.p_dropout > 0.f;
-  const bool big = p.B > kPlanCap;
+  // plan and item table in shared memory, else the global plan decoded per item
+  const bool big = !item_table_fits(p.B, max_items, grid);
   auto kern = drop ? (big ? bwd::fmha_bwd_kernel<true, true> : bwd::fmha_bwd_kernel<true, false>)
                    : (big ? bwd::fmha_bwd_kernel<false, true> : bwd::fmha_bwd_kernel<false, false>);
   {
@@ -638,7 +651,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
                            (uint64_t)3 * p.heads * bwd::kD * 2, 64, 32, 128)) != UB_OK)
     return st;
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
-  if (p.B > kPlanCap && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 0, v, s)) != UB_OK) return st;
+  if (big && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 0, v, s)) != UB_OK) return st;
   const int64_t rows = p.T * p.heads;
   launch_pdl(bwd::bwd_pre_kernel, dim3((unsigned)((rows * 8 + 255) / 256)), dim3(256), 0, s,
              static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), delta, p.T, p.heads);
@@ -662,12 +675,6 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   prm.k0 = (uint32_t)(p.seed & 0xFFFFFFFFull);
   prm.k1 = (uint32_t)(p.seed >> 32);
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t max_items = (int64_t)p.heads * p.B;
-  const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
-  const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfBwd, 0, s);
   launch_pdl(kern, dim3(grid), dim3(bwd::kThreads), bwd::kSmemBytes, s, tq, tdo, tdq, tdkv, prm);
   UB_CHECK_LAUNCH();

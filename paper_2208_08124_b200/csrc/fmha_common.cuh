@@ -142,6 +142,48 @@ __device__ __forceinline__ int32_t snake_item(int32_t r, int32_t c, int32_t G) {
   return r * G + ((r & 1) ? (G - 1 - c) : c);
 }
 
+// The CTA's work items, decoded once at kernel start (one warp) into shared memory: the
+// persistent loops then fetch item r with two shared loads instead of running the plan
+// decode (binary search + divisions) at every item boundary -- code that executes once per
+// item and so is rarely in the instruction cache.  The host guarantees that every CTA's
+// items fit (item_table_fits); otherwise it launches the kBigB form, which decodes per item.
+constexpr int kItemCap = 64;
+struct ItemTable {
+  int32_t n;                                   // this CTA's items
+  WorkItem it[kItemCap];
+};
+// host: every CTA's share in snake order (at most ceil(items / grid)) fits the table;
+// max_items is an upper bound of the plan's items
+inline bool item_table_fits(int32_t B, int64_t max_items, int32_t grid) {
+  return B <= kPlanCap && (max_items + grid - 1) / grid <= kItemCap;
+}
+
+__device__ __forceinline__ void build_item_table(ItemTable& t, const PlanSmem& ps, const int32_t* __restrict__ cu,
+                                                 int32_t B, int32_t H, int32_t tiles_per_item, int32_t cta, int32_t G,
+                                                 uint32_t lane) {
+  const FmhaPlanView none{};
+  int32_t count = 0;
+  for (int32_t r0 = 0; r0 < kItemCap; r0 += 32) {
+    const int32_t r = r0 + (int32_t)lane;
+    WorkItem it;
+    const bool ok = decode_item_smem<false>(snake_item(r, cta, G), ps, none, cu, B, H, tiles_per_item, it);
+    if (ok) t.it[r] = it;
+    count += __popc(__ballot_sync(0xffffffffu, ok));     // ok is monotone in r
+  }
+  if (lane == 0) t.n = count;
+}
+
+// item r of this CTA: from the table, or (kBigB) decoded from the global plan
+template <bool kBigB>
+__device__ __forceinline__ bool next_item(int32_t r, const ItemTable& t, const FmhaPlanView& v,
+                                          const int32_t* __restrict__ cu, int32_t B, int32_t H, int32_t tiles_per_item,
+                                          int32_t cta, int32_t G, WorkItem& it) {
+  if (kBigB) return decode_item(snake_item(r, cta, G), v, cu, B, H, tiles_per_item, it);
+  if (r >= t.n) return false;
+  it = t.it[r];
+  return true;
+}
+
 // Dropout keep bits for 16 consecutive keys j0..j0+15 (j0 % 16 == 0) of packed row t (R5):
 // bit e set <=> byte e of the Philox block (word e >> 2, byte e & 3) >= thr (8-bit threshold).
 __device__ __forceinline__ uint32_t keep_bits16(uint32_t j0, uint32_t t, uint32_t h, uint32_t off, uint32_t k0,

@@ -66,8 +66,10 @@ struct Smem {
   uint64_t s_full[2], s_free[2], p_full[2], o_done[2];   // per warpgroup
   uint32_t tmem_base;
   PlanSmem plan;
+  ItemTable items;                                // this CTA's items, decoded once
 };
 constexpr size_t kSmemBytes = sizeof(Smem);
+static_assert(kSmemBytes <= 227 * 1024, "shared memory per CTA");
 
 struct Params {
   const int32_t* cu;
@@ -134,7 +136,11 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   }
   if (warp == 9) tmem_alloc(&sm.tmem_base, 512);
   pdl_wait();                                            // everything below may read / write global memory
-  if (!kBigB && warp == 8) build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 2, lane);
+  if (!kBigB && warp == 8) {
+    build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 2, lane);
+    __syncwarp();
+    build_item_table(sm.items, sm.plan, prm.cu, prm.B, prm.H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, lane);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -150,7 +156,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     if (lane == 0) {
       uint32_t items = 0, kv_it = 0;
       WorkItem it;
-      for (int32_t r = 0; decode_item_smem<kBigB>(snake_item(r, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); ++r, ++items) {
+      for (int32_t r = 0; next_item<kBigB>(r, sm.items, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it); ++r, ++items) {
         const uint32_t slot = items & 1;
         TR(20);
         mbar_wait(&sm.q_empty[slot], ((items >> 1) & 1) ^ 1);
@@ -191,7 +197,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       };
       WorkItem it, nit;
       int32_t r = 0;                                      // this CTA's item round (snake order)
-      bool have = decode_item_smem<kBigB>(snake_item(0, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, it);
+      bool have = next_item<kBigB>(0, sm.items, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it);
       uint32_t items = 0, kv_it = 0;
       if (have) {
         mbar_wait(&sm.q_full[0], 0);
@@ -215,7 +221,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           if (j + 1 < it.nt) {
             nxt_tiles = nx;
           } else {
-            have_next_item = decode_item_smem<kBigB>(snake_item(r + 1, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, nit);
+            have_next_item = next_item<kBigB>(r + 1, sm.items, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, nit);
             if (have_next_item) {
               nxt_tiles = nit.ntile;
               nslot = slot ^ 1u;
@@ -335,7 +341,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       TR(9);
     };
     WorkItem it;
-    for (int32_t ri = 0; decode_item_smem<kBigB>(snake_item(ri, (int32_t)blockIdx.x, (int32_t)gridDim.x), sm.plan, prm.plan, prm.cu, prm.B, H, 2, it); ++ri) {
+    for (int32_t ri = 0; next_item<kBigB>(ri, sm.items, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it); ++ri) {
       if (x >= it.ntile) continue;
       const int32_t row = (it.tile + x) * kTile + (int32_t)r;
       const uint32_t t_glob = (uint32_t)(it.c0 + row);
@@ -512,7 +518,14 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   // tuning knob: fraction (x/8) of exp2 pairs on the FMA pipe, 0 or 2 (measured default 2)
   // measured on config 2: 0 -> 64.5 us, 2 -> 58.4, 3 -> 62.2, 4 -> 68.4 (issue-bound beyond 2/8)
   static const int poly = env_int("UB_FWD_POLY", 2, 0, 4) >= 2 ? 2 : 0;
-  const bool drop = p.p_dropout > 0.f, big = p.B > kPlanCap;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t max_items = (int64_t)p.heads * (p.B + p.T / (2 * kTile) + 1);   // >= sum_b ceil(nt_b / 2) * H
+  const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
+  const int grid = (int)std::min<int64_t>(ctas, max_items);
+  // plan and item table in shared memory, else the global plan decoded per item
+  const bool drop = p.p_dropout > 0.f, big = !item_table_fits(p.B, max_items, grid);
   void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params) = poly == 2 ? pick_fwd<2>(drop, big) : pick_fwd<0>(drop, big);
   {
     const ub_status sa = smem_attr_once(reinterpret_cast<const void*>(kern), (int)fwd::kSmemBytes);
@@ -532,7 +545,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
     return st;
   FmhaPlanView v = fmha_plan_view(ws, p.B);
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
-  if (p.B > kPlanCap && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 2, v, s)) != UB_OK) return st;
+  if (big && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 2, v, s)) != UB_OK) return st;
 
   fwd::Params prm{};
   prm.padded = static_cast<__nv_bfloat16*>(padded);
@@ -553,12 +566,6 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   prm.k1 = (uint32_t)(p.seed >> 32);
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
 
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t max_items = (int64_t)p.heads * (p.B + p.T / (2 * kTile) + 1);
-  const int ctas = p.num_ctas > 0 ? std::min(p.num_ctas, sms) : sms;
-  const int grid = (int)std::min<int64_t>(ctas, max_items);
   prof_record(kProfFwd, 0, s);
   launch_pdl(kern, dim3(grid), dim3(fwd::kThreads), fwd::kSmemBytes, s, tmap, tmap_out, tmap_pad, prm);
   UB_CHECK_LAUNCH();

@@ -174,6 +174,25 @@ def test_bf16_more_sequences_than_smem_plan(ub):
             assert_close(d[s:e, i].float().numpy(), dq[:, i], f"d{name} seq{b}")
 
 
+def test_item_table_overflow_same_results(ub):
+    """With 2 CTAs every CTA owns more items than its shared-memory item table holds, so the
+    kernels take the global-plan decode path: forward and backward must be bitwise the same
+    as with the full grid (the per-item arithmetic does not depend on the CTA)."""
+    rng = np.random.default_rng(11)
+    L = rng.integers(1, 513, size=40).astype(np.int32)
+    lengths, off, qkv, dout = make_batch(L, 4, 64, seed=5)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    qd, gd = qkv.cuda(), dout.cuda()
+    res = []
+    for n in (0, 2):
+        o, lse = ub.varlen_fmha_fwd(qd, cu, 512, num_ctas=n)
+        d = ub.varlen_fmha_bwd(qd, o, lse, gd, cu, 512, num_ctas=n)
+        torch.cuda.synchronize()
+        res.append((o.cpu(), lse.cpu(), d.cpu()))
+    for a, b in zip(res[0], res[1]):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("p", [0.0, 0.1])
 def test_fwd_with_fused_pad(ub, p):
     """ub_varlen_fmha_fwd_pad (a7 + a9): out / lse identical to the plain forward, padded
