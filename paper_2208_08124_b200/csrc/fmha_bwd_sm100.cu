@@ -167,7 +167,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   const int32_t H = prm.H;
   const int32_t G = (int32_t)gridDim.x, cta = (int32_t)blockIdx.x;
 #define UB_ITEMS(r, it) \
-  for (int32_t r = 0; next_item<kBigB>(r, sm.items, prm.plan, prm.cu, prm.B, H, 0, cta, G, it); ++r)
+  for (int32_t r = 0; next_item<kBigB>(r, sm.items, sm.plan, prm.plan, prm.cu, prm.B, H, 0, cta, G, it); ++r)
   // each role re-sizes its registers at its entry, inside its branch (ptxas takes the
   // minimum where paths merge); setmaxnreg is warpgroup-uniform
 

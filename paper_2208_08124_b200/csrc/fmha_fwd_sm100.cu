@@ -156,7 +156,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     if (lane == 0) {
       uint32_t items = 0, kv_it = 0;
       WorkItem it;
-      for (int32_t r = 0; next_item<kBigB>(r, sm.items, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it); ++r, ++items) {
+      for (int32_t r = 0; next_item<kBigB, !kDropout>(r, sm.items, sm.plan, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it); ++r, ++items) {
         const uint32_t slot = items & 1;
         TR(20);
         mbar_wait(&sm.q_empty[slot], ((items >> 1) & 1) ^ 1);
@@ -197,7 +197,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       };
       WorkItem it, nit;
       int32_t r = 0;                                      // this CTA's item round (snake order)
-      bool have = next_item<kBigB>(0, sm.items, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it);
+      bool have = next_item<kBigB, !kDropout>(0, sm.items, sm.plan, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it);
       uint32_t items = 0, kv_it = 0;
       if (have) {
         mbar_wait(&sm.q_full[0], 0);
@@ -221,7 +221,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           if (j + 1 < it.nt) {
             nxt_tiles = nx;
           } else {
-            have_next_item = next_item<kBigB>(r + 1, sm.items, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, nit);
+            have_next_item = next_item<kBigB, !kDropout>(r + 1, sm.items, sm.plan, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, nit);
             if (have_next_item) {
               nxt_tiles = nit.ntile;
               nslot = slot ^ 1u;
@@ -341,7 +341,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       TR(9);
     };
     WorkItem it;
-    for (int32_t ri = 0; next_item<kBigB>(ri, sm.items, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it); ++ri) {
+    for (int32_t ri = 0; next_item<kBigB, !kDropout>(ri, sm.items, sm.plan, prm.plan, prm.cu, prm.B, H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, it); ++ri) {
       if (x >= it.ntile) continue;
       const int32_t row = (it.tile + x) * kTile + (int32_t)r;
       const uint32_t t_glob = (uint32_t)(it.c0 + row);
