@@ -28,7 +28,8 @@
 //   warp 13     TMEM allocator, then MMA issuer (one thread)
 //   warp 14     producer of K, V per pass (double-buffered); warp 15 idle
 // Registers: 128 per thread at launch; setmaxnreg moves them to the compute warpgroups
-// (168) and the epilogue (120) from the producer / MMA warps (56): 2 x 168 + 120 + 56 = 4 x 128.
+// (168) and the epilogue (112) from the producer / MMA warps (64): 2 x 168 + 112 + 64 = 4 x 128
+// (64 rather than 56 for the MMA issuer: 20 -> 6 spill instructions, -1 % time).
 // TMEM columns: S^T 0..127, dP^T 128..255, P~^T 256..319 (bf16 pairs), dQ 320..383,
 // dV 384..447, dK 448..511.
 // The MMA issues S_{p+1}, dP_{p+1} as soon as the compute warps have loaded S_p, dP_p, so
@@ -172,7 +173,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   // minimum where paths merge); setmaxnreg is warpgroup-uniform
 
   if (warp >= 12) {
-    regs_dec<56>();
+    regs_dec<64>();
   }
   if (warp == 14) {
     // ------------------------------------------------------------ K / V producer (per pass)
@@ -399,7 +400,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     }
   } else if (warp < 12) {
     // ------------------------------------------------------------ epilogue warpgroup
-    regs_dec<120>();
+    regs_dec<112>();
     const uint32_t qd = warp & 3;                           // TMEM lane quadrant
     const uint32_t t_row = tmem + ((qd * 32) << 16);
     uint8_t* stage = sm.stage[qd];
