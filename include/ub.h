@@ -298,6 +298,42 @@ ub_status ub_exchange_copy(const void* src_tokens, void* dst_tokens, const void*
                            void* dst_samples, const int64_t* d_tab, int32_t B, int64_t rec_bytes,
                            int64_t srec_bytes, void* stream);
 
+/* ------------------------------------------------------------------------------------
+ * Pull-based exchange (the data movement of P:355-359 step 3 done as
+ * one gather): every rank copies its perm-ordered samples directly out of the peers'
+ * packed token buffers, mapped into its address space by CUDA IPC -- the all-to-all-v
+ * (a4) and the reorder (a5) in one kernel, no staging buffers, no NCCL kernels.
+ *
+ * ub_ipc_export (host): writes UB_IPC_HANDLE_BYTES bytes describing the device buffer that
+ *   starts at d_ptr (the CUDA IPC handle of its allocation plus d_ptr's offset in it), to be
+ *   sent to the other ranks (e.g. over torch.distributed).  d_ptr must come from cudaMalloc
+ *   (directly or through a caching allocator).  Errors: not device memory -> INVALID_ARG.
+ * ub_ipc_import (host): maps a peer's exported buffer; *d_ptr = the buffer in this process,
+ *   *d_base = the mapping to pass to ub_ipc_close when done.  A handle exported by this
+ *   process cannot be imported by it (CUDA returns an error -> UB_ERR_CUDA).
+ * ub_exchange_pull_table (host): for rank `rank`, from the all-gathered lengths and the plan
+ *   (perm as ub_balance_plan writes it), h_tab [6*B] int64 = {src_rank[B], src_tok[B],
+ *   len[B], dst_tok[B], src_smp[B], dst_smp[B]}: output sample k (perm order) is local
+ *   sample src_smp of rank src_rank, whose token records start at record src_tok of that
+ *   rank's packed buffer (its local cu_seqlens); it lands at record dst_tok.
+ *   *h_total_tokens (may be NULL) = records this rank receives.  Errors: perm not a
+ *   permutation -> SHAPE; negative length -> INVALID_ARG.
+ * ub_exchange_pull (device, async on `stream`): d_peer_tokens / d_peer_samples are DEVICE
+ *   arrays of W pointers (this rank's own buffers at its own index), each 16-B aligned when
+ *   rec_bytes % 16 == 0; d_tab is the pull table in device memory.  One CTA per output
+ *   sample.  The caller orders the peers' writes of their buffers before this call and this
+ *   call before the peers' next writes (events or a barrier: the library does not).
+ */
+#define UB_IPC_HANDLE_BYTES 128
+ub_status ub_ipc_export(const void* d_ptr, void* h_handle);
+ub_status ub_ipc_import(const void* h_handle, void** d_ptr, void** d_base);
+ub_status ub_ipc_close(void* d_base);
+ub_status ub_exchange_pull_table(const int32_t* h_all_lengths, const int32_t* h_perm, int32_t W,
+                                 int32_t B, int32_t rank, int64_t* h_tab, int64_t* h_total_tokens);
+ub_status ub_exchange_pull(const void* const* d_peer_tokens, const void* const* d_peer_samples,
+                           const int64_t* d_tab, int32_t B, int64_t rec_bytes, int64_t srec_bytes,
+                           void* dst_tokens, void* dst_samples, void* stream);
+
 /* NCCL communicator (NCCL over NVLink 5 / NVSwitch).  nccl_unique_id: the 128-byte
  * ncclUniqueId produced by ub_comm_unique_id() on rank 0 and broadcast by the caller
  * (e.g. over a torch.distributed process group).  Must be called with the CUDA device

@@ -12,6 +12,7 @@ UB_OK = 0
 STATUS_NAMES = {0: "UB_OK", 1: "UB_ERR_INVALID_ARG", 2: "UB_ERR_INVALID_MASK", 3: "UB_ERR_CAPACITY",
                 4: "UB_ERR_SHAPE", 5: "UB_ERR_UNSUPPORTED", 6: "UB_ERR_CUDA", 7: "UB_ERR_NCCL"}
 UB_BF16, UB_FP32 = 0, 1
+UB_IPC_HANDLE_BYTES = 128
 UB_BAL_PAPER, UB_BAL_SNAKE, UB_BAL_EXACT_SMALL, UB_BAL_LPT = 0, 1, 2, 3
 
 # every symbol include/ub.h declares, with (restype, argtypes)
@@ -57,6 +58,11 @@ SIGNATURES = {
     "ub_balance_plan_weighted": (i32, [vp, i32, i32, i32, i64, i64, vp, vp]),
     "ub_exchange_tables": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
     "ub_exchange_copy": (i32, [vp, vp, vp, vp, vp, i32, i64, i64, vp]),
+    "ub_ipc_export": (i32, [vp, vp]),
+    "ub_ipc_import": (i32, [vp, vp, vp]),
+    "ub_ipc_close": (i32, [vp]),
+    "ub_exchange_pull_table": (i32, [vp, vp, i32, i32, i32, vp, vp]),
+    "ub_exchange_pull": (i32, [vp, vp, vp, i32, i64, i64, vp, vp, vp]),
     "ub_comm_unique_id": (i32, [vp]),
     "ub_comm_init": (i32, [C.POINTER(vp), vp, i32, i32]),
     "ub_comm_destroy": (i32, [vp]),

@@ -12,7 +12,8 @@ import math
 import numpy as np
 import torch
 
-from ._lib import (EncoderParams, UB_BAL_EXACT_SMALL, UB_BAL_LPT, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BF16, UB_FP32, FmhaParams, check, lib)
+from ._lib import (EncoderParams, UB_BAL_EXACT_SMALL, UB_BAL_LPT, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BF16, UB_FP32,
+                   UB_IPC_HANDLE_BYTES, FmhaParams, check, lib)
 
 BAL_MODES = {"paper": UB_BAL_PAPER, "snake": UB_BAL_SNAKE, "exact_small": UB_BAL_EXACT_SMALL, "lpt": UB_BAL_LPT}
 
@@ -301,6 +302,44 @@ def exchange_tables(all_lengths, perm, W: int, B: int, rank: int, unpack: bool):
 def exchange_copy(src_tokens, dst_tokens, src_samples, dst_samples, d_tab, B, rec_bytes, srec_bytes, stream=None):
     check(lib().ub_exchange_copy(_ptr(src_tokens), _ptr(dst_tokens), _ptr(src_samples), _ptr(dst_samples),
                                  _ptr(d_tab), B, int(rec_bytes), int(srec_bytes), _stream(stream)))
+
+
+# ------------------------------------------------------------------ pull exchange (NEXT-3)
+def ipc_export(t: torch.Tensor) -> bytes:
+    """Handle (UB_IPC_HANDLE_BYTES) of the device buffer starting at t, for the other ranks."""
+    buf = (C.c_uint8 * UB_IPC_HANDLE_BYTES)()
+    check(lib().ub_ipc_export(_ptr(t), C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def ipc_import(handle: bytes):
+    """Maps a peer's exported buffer: returns (device pointer, mapping base for ipc_close)."""
+    raw = (C.c_uint8 * UB_IPC_HANDLE_BYTES)(*handle)
+    ptr, base = C.c_void_p(), C.c_void_p()
+    check(lib().ub_ipc_import(C.cast(raw, C.c_void_p), C.byref(ptr), C.byref(base)))
+    return ptr.value, base.value
+
+
+def ipc_close(base: int):
+    check(lib().ub_ipc_close(C.c_void_p(base)))
+
+
+def exchange_pull_table(all_lengths, perm, W: int, B: int, rank: int):
+    """Pull table [6*B] int64 of rank `rank` (see include/ub.h) and its received records."""
+    a = np.ascontiguousarray(np.asarray(all_lengths, dtype=np.int32).reshape(-1))
+    p = np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    tab = np.zeros(6 * B, dtype=np.int64)
+    total = np.zeros(1, dtype=np.int64)
+    check(lib().ub_exchange_pull_table(_np_ptr(a), _np_ptr(p), W, B, rank, _np_ptr(tab), _np_ptr(total)))
+    return tab, int(total[0])
+
+
+def exchange_pull(d_peer_tokens: torch.Tensor, d_peer_samples, d_tab: torch.Tensor, B: int, rec_bytes: int,
+                  srec_bytes: int, out_tokens: torch.Tensor, out_samples=None, stream=None):
+    """d_peer_tokens / d_peer_samples: int64 CUDA tensors [W] of device pointers."""
+    check(lib().ub_exchange_pull(_ptr(d_peer_tokens), _ptr(d_peer_samples) if d_peer_samples is not None else None,
+                                 _ptr(d_tab), B, int(rec_bytes), int(srec_bytes), _ptr(out_tokens),
+                                 _ptr(out_samples) if out_samples is not None else None, _stream(stream)))
 
 
 class Comm:

@@ -157,3 +157,31 @@ def test_exchange_tables_reproduce_oracle_exchange(ub):
         out_t, out_s = apply(tab, recv_t, recv_s, tot)
         assert np.array_equal(out_t, exp[d]["tokens"])
         assert np.array_equal(out_s, exp[d]["samples"])
+
+
+@pytest.mark.parametrize("W,B", [(1, 5), (2, 7), (4, 7), (8, 3)])
+def test_exchange_pull_table_reproduces_oracle_exchange(ub, W, B):
+    """NEXT-3: apply the pull table (each output sample copied straight out of its source
+    rank's packed batch) with numpy and compare every rank's bytes with the oracle."""
+    from paper_2208_08124_b200 import api
+    rec, srec = 16, 4
+    lens = synth.gen_lengths("mlperf_like_v0", W * B, 10 + W).reshape(W, B)
+    toks = [synth.gen_bytes(int(lens[r].sum()) * rec, 70 + r).reshape(-1, rec) for r in range(W)]
+    smps = [synth.gen_bytes(B * srec, 80 + r).reshape(B, srec) for r in range(W)]
+    plan = api.balance_plan(lens.reshape(-1), W, B, 512, "paper")
+    exp = oex.exchange(lens, toks, smps, plan["perm"], W, B)
+    for d in range(W):
+        tab, tot = api.exchange_pull_table(lens.reshape(-1), plan["perm"], W, B, d)
+        assert tot == plan["rank_tokens"][d]
+        out_t = np.zeros((tot, rec), np.uint8)
+        out_s = np.zeros((B, srec), np.uint8)
+        for e in range(B):
+            src, s0, n, d0, ss, ds = (int(tab[k * B + e]) for k in range(6))
+            out_t[d0:d0 + n] = toks[src][s0:s0 + n]
+            out_s[ds] = smps[src][ss]
+        assert np.array_equal(out_t, exp[d]["tokens"]) and np.array_equal(out_s, exp[d]["samples"])
+    from paper_2208_08124_b200 import UbError
+    bad = plan["perm"].copy()
+    bad[0] = bad[1]
+    with pytest.raises(UbError):
+        api.exchange_pull_table(lens.reshape(-1), bad, W, B, 0)
