@@ -321,8 +321,16 @@ ub_status ub_exchange_copy(const void* src_tokens, void* dst_tokens, const void*
  * ub_exchange_pull (device, async on `stream`): d_peer_tokens / d_peer_samples are DEVICE
  *   arrays of W pointers (this rank's own buffers at its own index), each 16-B aligned when
  *   rec_bytes % 16 == 0; d_tab is the pull table in device memory.  One CTA per output
- *   sample.  The caller orders the peers' writes of their buffers before this call and this
- *   call before the peers' next writes (events or a barrier: the library does not).
+ *   sample.  d_ready (may be NULL): DEVICE array of W pointers to the ranks' "buffer
+ *   published" flags (IPC-mapped); each CTA first waits, with system-scope acquire, until
+ *   the flag of its source rank is >= wait_value, so the host never waits.  Without flags
+ *   the caller orders the peers' writes before the call (a barrier).
+ * ub_signal (device, async): after every earlier write of `stream`, stores `value` to the
+ *   uint32 flag with system-scope release (a rank publishes its buffer, or its completed
+ *   pull, to the other processes).
+ * ub_wait_flags (device, async): `stream` waits until each of the n flags (DEVICE array of
+ *   pointers) is >= value, e.g. before overwriting a buffer the peers may still be reading.
+ *   Flags are monotone counters (a step number); the waits spin on the GPU, one CTA.
  */
 #define UB_IPC_HANDLE_BYTES 128
 ub_status ub_ipc_export(const void* d_ptr, void* h_handle);
@@ -331,8 +339,11 @@ ub_status ub_ipc_close(void* d_base);
 ub_status ub_exchange_pull_table(const int32_t* h_all_lengths, const int32_t* h_perm, int32_t W,
                                  int32_t B, int32_t rank, int64_t* h_tab, int64_t* h_total_tokens);
 ub_status ub_exchange_pull(const void* const* d_peer_tokens, const void* const* d_peer_samples,
-                           const int64_t* d_tab, int32_t B, int64_t rec_bytes, int64_t srec_bytes,
-                           void* dst_tokens, void* dst_samples, void* stream);
+                           const uint32_t* const* d_ready, uint32_t wait_value, const int64_t* d_tab,
+                           int32_t B, int64_t rec_bytes, int64_t srec_bytes, void* dst_tokens,
+                           void* dst_samples, void* stream);
+ub_status ub_signal(uint32_t* d_flag, uint32_t value, void* stream);
+ub_status ub_wait_flags(const uint32_t* const* d_flags, int32_t n, uint32_t value, void* stream);
 
 /* NCCL communicator (NCCL over NVLink 5 / NVSwitch).  nccl_unique_id: the 128-byte
  * ncclUniqueId produced by ub_comm_unique_id() on rank 0 and broadcast by the caller

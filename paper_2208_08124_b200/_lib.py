@@ -62,7 +62,9 @@ SIGNATURES = {
     "ub_ipc_import": (i32, [vp, vp, vp]),
     "ub_ipc_close": (i32, [vp]),
     "ub_exchange_pull_table": (i32, [vp, vp, i32, i32, i32, vp, vp]),
-    "ub_exchange_pull": (i32, [vp, vp, vp, i32, i64, i64, vp, vp, vp]),
+    "ub_exchange_pull": (i32, [vp, vp, vp, C.c_uint32, vp, i32, i64, i64, vp, vp, vp]),
+    "ub_signal": (i32, [vp, C.c_uint32, vp]),
+    "ub_wait_flags": (i32, [vp, i32, C.c_uint32, vp]),
     "ub_comm_unique_id": (i32, [vp]),
     "ub_comm_init": (i32, [C.POINTER(vp), vp, i32, i32]),
     "ub_comm_destroy": (i32, [vp]),

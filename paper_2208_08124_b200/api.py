@@ -335,11 +335,22 @@ def exchange_pull_table(all_lengths, perm, W: int, B: int, rank: int):
 
 
 def exchange_pull(d_peer_tokens: torch.Tensor, d_peer_samples, d_tab: torch.Tensor, B: int, rec_bytes: int,
-                  srec_bytes: int, out_tokens: torch.Tensor, out_samples=None, stream=None):
-    """d_peer_tokens / d_peer_samples: int64 CUDA tensors [W] of device pointers."""
-    check(lib().ub_exchange_pull(_ptr(d_peer_tokens), _ptr(d_peer_samples) if d_peer_samples is not None else None,
-                                 _ptr(d_tab), B, int(rec_bytes), int(srec_bytes), _ptr(out_tokens),
-                                 _ptr(out_samples) if out_samples is not None else None, _stream(stream)))
+                  srec_bytes: int, out_tokens: torch.Tensor, out_samples=None, d_ready=None, wait_value: int = 0,
+                  stream=None):
+    """d_peer_tokens / d_peer_samples / d_ready: int64 CUDA tensors [W] of device pointers."""
+    check(lib().ub_exchange_pull(_ptr(d_peer_tokens), _ptr(d_peer_samples), _ptr(d_ready), int(wait_value),
+                                 _ptr(d_tab), B, int(rec_bytes), int(srec_bytes), _ptr(out_tokens), _ptr(out_samples),
+                                 _stream(stream)))
+
+
+def signal(flag: torch.Tensor, value: int, stream=None):
+    """flag: a uint32 / int32 CUDA tensor element (its first element is set)."""
+    check(lib().ub_signal(_ptr(flag), int(value), _stream(stream)))
+
+
+def wait_flags(d_flags: torch.Tensor, value: int, stream=None):
+    """d_flags: int64 CUDA tensor [n] of device pointers to uint32 flags."""
+    check(lib().ub_wait_flags(_ptr(d_flags), int(d_flags.numel()), int(value), _stream(stream)))
 
 
 class Comm:

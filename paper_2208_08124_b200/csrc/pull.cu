@@ -18,17 +18,36 @@
 
 namespace ub {
 
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void spin_until_ge(const uint32_t* p, uint32_t v) {
+  while (ld_acquire_sys(p) < v) __nanosleep(256);
+}
+
 // One CTA per output sample: len * rec bytes of token records from the source rank's
 // buffer, srec bytes of its sample record.  tab = {src_rank, src_tok, len, dst_tok,
-// src_smp, dst_smp} x B.
+// src_smp, dst_smp} x B.  With ready flags, a CTA first waits (acquire, system scope) until
+// its source rank has published the buffer (ready[src] >= wait_value): a sample moves as soon
+// as its own source is ready.
 template <typename Vec>
 __global__ void __launch_bounds__(256) exchange_pull_kernel(const uint8_t* const* __restrict__ peer_tok,
                                                             const uint8_t* const* __restrict__ peer_smp,
-                                                            uint8_t* __restrict__ dt, uint8_t* __restrict__ ds,
-                                                            const int64_t* __restrict__ tab, int32_t B, int64_t rec,
-                                                            int64_t srec) {
+                                                            const uint32_t* const* __restrict__ ready,
+                                                            uint32_t wait_value, uint8_t* __restrict__ dt,
+                                                            uint8_t* __restrict__ ds, const int64_t* __restrict__ tab,
+                                                            int32_t B, int64_t rec, int64_t srec) {
   const int e = blockIdx.x;
   const int64_t src = tab[e], src_tok = tab[B + e], len = tab[2 * B + e], dst_tok = tab[3 * B + e];
+  if (ready != nullptr) {
+    if (threadIdx.x == 0) spin_until_ge(ready[src], wait_value);
+    __syncthreads();
+  }
   const Vec* s = reinterpret_cast<const Vec*>(peer_tok[src] + src_tok * rec);
   Vec* d = reinterpret_cast<Vec*>(dt + dst_tok * rec);
   const int64_t nv = len * rec / (int64_t)sizeof(Vec);
@@ -38,6 +57,18 @@ __global__ void __launch_bounds__(256) exchange_pull_kernel(const uint8_t* const
     uint8_t* dd = ds + tab[5 * B + e] * srec;
     for (int64_t i = threadIdx.x; i < srec; i += blockDim.x) dd[i] = ss[i];
   }
+}
+
+// publish: every earlier write of this stream is visible system-wide before the flag
+__global__ void signal_kernel(uint32_t* flag, uint32_t value) {
+  __threadfence_system();
+  st_release_sys(flag, value);
+}
+// wait until flags[i] >= value for all i < n (one thread per flag)
+__global__ void wait_flags_kernel(const uint32_t* const* __restrict__ flags, int32_t n, uint32_t value) {
+  for (int32_t i = threadIdx.x; i < n; i += blockDim.x) spin_until_ge(flags[i], value);
+  __syncthreads();
+  __threadfence_system();
 }
 
 // export: the CUDA IPC handle of the allocation holding ptr, plus ptr's offset in it (a
@@ -133,8 +164,9 @@ extern "C" ub_status ub_exchange_pull_table(const int32_t* a, const int32_t* per
 }
 
 extern "C" ub_status ub_exchange_pull(const void* const* d_peer_tokens, const void* const* d_peer_samples,
-                                      const int64_t* d_tab, int32_t B, int64_t rec_bytes, int64_t srec_bytes,
-                                      void* dst_tokens, void* dst_samples, void* stream) {
+                                      const uint32_t* const* d_ready, uint32_t wait_value, const int64_t* d_tab,
+                                      int32_t B, int64_t rec_bytes, int64_t srec_bytes, void* dst_tokens,
+                                      void* dst_samples, void* stream) {
   clear_error();
   UB_REQUIRE(d_peer_tokens && d_tab && dst_tokens, UB_ERR_INVALID_ARG, "null pointer");
   UB_REQUIRE(B >= 1 && rec_bytes > 0 && srec_bytes >= 0, UB_ERR_SHAPE, "bad sizes");
@@ -146,11 +178,29 @@ extern "C" ub_status ub_exchange_pull(const void* const* d_peer_tokens, const vo
   auto* ds = static_cast<uint8_t*>(dst_samples);
   // peer buffers are the callers' (16-B aligned allocations); the vector width follows rec
   if (rec_bytes % 16 == 0 && ((uintptr_t)dst_tokens & 15) == 0)
-    exchange_pull_kernel<int4><<<B, 256, 0, s>>>(pt, ps, dt, ds, d_tab, B, rec_bytes, srec_bytes);
+    exchange_pull_kernel<int4><<<B, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes, srec_bytes);
   else if (rec_bytes % 4 == 0 && ((uintptr_t)dst_tokens & 3) == 0)
-    exchange_pull_kernel<uint32_t><<<B, 256, 0, s>>>(pt, ps, dt, ds, d_tab, B, rec_bytes, srec_bytes);
+    exchange_pull_kernel<uint32_t><<<B, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes,
+                                                      srec_bytes);
   else
-    exchange_pull_kernel<uint8_t><<<B, 256, 0, s>>>(pt, ps, dt, ds, d_tab, B, rec_bytes, srec_bytes);
+    exchange_pull_kernel<uint8_t><<<B, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes,
+                                                     srec_bytes);
+  UB_CHECK_LAUNCH();
+  return UB_OK;
+}
+
+extern "C" ub_status ub_signal(uint32_t* d_flag, uint32_t value, void* stream) {
+  clear_error();
+  UB_REQUIRE(d_flag, UB_ERR_INVALID_ARG, "null pointer");
+  signal_kernel<<<1, 1, 0, as_stream(stream)>>>(d_flag, value);
+  UB_CHECK_LAUNCH();
+  return UB_OK;
+}
+
+extern "C" ub_status ub_wait_flags(const uint32_t* const* d_flags, int32_t n, uint32_t value, void* stream) {
+  clear_error();
+  UB_REQUIRE(d_flags && n >= 1, UB_ERR_INVALID_ARG, "bad flags");
+  wait_flags_kernel<<<1, 32, 0, as_stream(stream)>>>(d_flags, n, value);
   UB_CHECK_LAUNCH();
   return UB_OK;
 }
