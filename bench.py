@@ -576,6 +576,38 @@ def gather_bench(wl, peaks, iters=20):
         out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
                      "bytes": int(nbytes)}
     out["shape"] = f"hidden [{B}, {S}, {H * D}] bf16 <-> [T={T}, {H * D}]"
+    # NEXT-3: the exchange's data movement at SURVEY §8(a) a4's stress record size (a bf16
+    # hidden row, 2 kB per token), one rank: the pull gather (one pass) against the NCCL
+    # path's pack + unpack copies (two passes; the transport between them is a third)
+    rec = H * D * 2
+    lens = np.asarray(st["L"], np.int32)
+    perm = api.balance_plan(lens, 1, B, S, "paper")["perm"]
+    d_pack = torch.from_numpy(api.exchange_tables(lens, perm, 1, B, 0, unpack=False)[0]).to(wl.dev)
+    d_unpack = torch.from_numpy(api.exchange_tables(lens, perm, 1, B, 0, unpack=True)[0]).to(wl.dev)
+    d_pull = torch.from_numpy(api.exchange_pull_table(lens, perm, 1, B, 0)[0]).to(wl.dev)
+    src = [torch.randint(0, 255, (T, rec), dtype=torch.uint8, device=wl.dev) for _ in range(3)]
+    mid = torch.empty((T, rec), dtype=torch.uint8, device=wl.dev)
+    dst = torch.empty((T, rec), dtype=torch.uint8, device=wl.dev)
+    peers = [torch.tensor([x.data_ptr()], dtype=torch.int64, device=wl.dev) for x in src]
+    for name, fn, nbytes in (
+            ("exchange_2kB_pull", lambda k: api.exchange_pull(peers[k], None, d_pull, B, rec, 0, dst), 2 * T * rec),
+            ("exchange_2kB_pack_unpack", lambda k: (api.exchange_copy(src[k], mid, None, None, d_pack, B, rec, 0),
+                                                    api.exchange_copy(mid, dst, None, None, d_unpack, B, rec, 0)),
+             4 * T * rec)):
+        for k in range(3):
+            fn(k)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        torch.cuda._sleep(2_000_000)
+        for k in range(iters):
+            ev[k][0].record()
+            fn(k % 3)
+            ev[k][1].record()
+        torch.cuda.synchronize()
+        us = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
+        gbs = nbytes / (us * 1e-6) / 1e9
+        out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
+                     "bytes": int(nbytes), "rec_bytes": rec, "ranks": 1}
     # NEXT-1 piece: Dropout_Add_LayerNorm on the same packed hidden state, p = 0.1
     E = H * D
     hs = [tuple(torch.randn((T, E), device=wl.dev).to(torch.bfloat16) for _ in range(3)) for _ in range(3)]

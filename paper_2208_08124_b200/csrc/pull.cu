@@ -51,8 +51,10 @@ __global__ void __launch_bounds__(256) exchange_pull_kernel(const uint8_t* const
   const Vec* s = reinterpret_cast<const Vec*>(peer_tok[src] + src_tok * rec);
   Vec* d = reinterpret_cast<Vec*>(dt + dst_tok * rec);
   const int64_t nv = len * rec / (int64_t)sizeof(Vec);
-  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d[i] = s[i];
-  if (srec > 0) {
+  // gridDim.y CTAs share a sample (large records): interleaved 256-vector blocks
+  for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.y * blockDim.x)
+    d[i] = s[i];
+  if (srec > 0 && blockIdx.y == 0) {
     const uint8_t* ss = peer_smp[src] + tab[4 * B + e] * srec;
     uint8_t* dd = ds + tab[5 * B + e] * srec;
     for (int64_t i = threadIdx.x; i < srec; i += blockDim.x) dd[i] = ss[i];
@@ -176,14 +178,16 @@ extern "C" ub_status ub_exchange_pull(const void* const* d_peer_tokens, const vo
   auto* ps = reinterpret_cast<const uint8_t* const*>(d_peer_samples);
   auto* dt = static_cast<uint8_t*>(dst_tokens);
   auto* ds = static_cast<uint8_t*>(dst_samples);
-  // peer buffers are the callers' (16-B aligned allocations); the vector width follows rec
+  // peer buffers are the callers' (16-B aligned allocations); the vector width follows rec.
+  // Large records (a hidden row per token): 16 CTAs per sample, else one.
+  const dim3 grid(B, rec_bytes >= 256 ? 16 : 1);
   if (rec_bytes % 16 == 0 && ((uintptr_t)dst_tokens & 15) == 0)
-    exchange_pull_kernel<int4><<<B, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes, srec_bytes);
+    exchange_pull_kernel<int4><<<grid, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes, srec_bytes);
   else if (rec_bytes % 4 == 0 && ((uintptr_t)dst_tokens & 3) == 0)
-    exchange_pull_kernel<uint32_t><<<B, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes,
+    exchange_pull_kernel<uint32_t><<<grid, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes,
                                                       srec_bytes);
   else
-    exchange_pull_kernel<uint8_t><<<B, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes,
+    exchange_pull_kernel<uint8_t><<<grid, 256, 0, s>>>(pt, ps, d_ready, wait_value, dt, ds, d_tab, B, rec_bytes,
                                                      srec_bytes);
   UB_CHECK_LAUNCH();
   return UB_OK;

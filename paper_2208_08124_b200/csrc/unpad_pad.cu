@@ -194,7 +194,7 @@ static ub_status unpad_pad_dispatch(bool pad, const void* src, void* dst, const 
 }
 
 // ------------------------------------------------------------------ exchange copy
-// One CTA per table entry: copies len*rec bytes of token records and srec bytes of the
+// One CTA (or gridDim.y CTAs) per table entry: copies len*rec bytes of token records and srec bytes of the
 // sample record.  tab = {src_tok[B], len[B], dst_tok[B], src_smp[B], dst_smp[B]}.
 template <typename Vec>
 __global__ void __launch_bounds__(256) exchange_copy_kernel(const uint8_t* __restrict__ st, uint8_t* __restrict__ dt,
@@ -206,8 +206,10 @@ __global__ void __launch_bounds__(256) exchange_copy_kernel(const uint8_t* __res
   const Vec* s = reinterpret_cast<const Vec*>(st + src_tok * rec);
   Vec* d = reinterpret_cast<Vec*>(dt + dst_tok * rec);
   const int64_t nv = len * rec / (int64_t)sizeof(Vec);
-  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d[i] = s[i];
-  if (srec > 0) {
+  // gridDim.y CTAs share an entry (large records): interleaved 256-vector blocks
+  for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.y * blockDim.x)
+    d[i] = s[i];
+  if (srec > 0 && blockIdx.y == 0) {
     const int64_t so = tab[3 * B + e] * srec, dso = tab[4 * B + e] * srec;
     for (int64_t i = threadIdx.x; i < srec; i += blockDim.x) ds[dso + i] = ss[so + i];
   }
@@ -240,12 +242,13 @@ extern "C" ub_status ub_exchange_copy(const void* src_tokens, void* dst_tokens, 
   auto* dt = static_cast<uint8_t*>(dst_tokens);
   auto* ss = static_cast<const uint8_t*>(src_samples);
   auto* ds = static_cast<uint8_t*>(dst_samples);
+  const dim3 grid(B, rec_bytes >= 256 ? 16 : 1);     // large records: 16 CTAs per entry
   if (rec_bytes % 16 == 0 && (al & 15) == 0)
-    exchange_copy_kernel<int4><<<B, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
+    exchange_copy_kernel<int4><<<grid, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
   else if (rec_bytes % 4 == 0 && (al & 3) == 0)
-    exchange_copy_kernel<uint32_t><<<B, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
+    exchange_copy_kernel<uint32_t><<<grid, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
   else
-    exchange_copy_kernel<uint8_t><<<B, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
+    exchange_copy_kernel<uint8_t><<<grid, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
   UB_CHECK_LAUNCH();
   return UB_OK;
 }
