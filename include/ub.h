@@ -299,6 +299,22 @@ ub_status ub_exchange_copy(const void* src_tokens, void* dst_tokens, const void*
                            int64_t srec_bytes, void* stream);
 
 /* ------------------------------------------------------------------------------------
+ * Checked mode (SURVEY §8(b) "Errors": device-resident data is not validated on the fast
+ * path; a debug switch validates it on the device and reports after a sync -- tests only).
+ *
+ * ub_validate_cu_seqlens (device, async): one CTA checks the device cu_seqlens [B+1] and
+ *   writes *d_flag (device int32): 0 valid, 1 cu[0] != 0, 2 not monotone, 3 a length >
+ *   max_seqlen, 4 cu[B] > T.  The caller reads the flag after synchronising.
+ * ub_set_checked (host): on != 0 makes ub_unpad / ub_pad (max_seqlen = S) and the FMHA
+ *   entry points run that check first, synchronise the stream and return CAPACITY (code 3)
+ *   or INVALID_ARG (codes 1, 2, 4) instead of launching.  Also switched on by UB_CHECKED=1
+ *   in the environment.  Off by default: it costs a host synchronisation per call.
+ */
+ub_status ub_validate_cu_seqlens(const int32_t* d_cu, int32_t B, int32_t max_seqlen, int64_t T,
+                                 int32_t* d_flag, void* stream);
+ub_status ub_set_checked(int32_t on);
+
+/* ------------------------------------------------------------------------------------
  * Pull-based exchange (the data movement of P:355-359 step 3 done as
  * one gather): every rank copies its perm-ordered samples directly out of the peers'
  * packed token buffers, mapped into its address space by CUDA IPC -- the all-to-all-v

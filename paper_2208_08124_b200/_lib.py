@@ -58,6 +58,8 @@ SIGNATURES = {
     "ub_balance_plan_weighted": (i32, [vp, i32, i32, i32, i64, i64, vp, vp]),
     "ub_exchange_tables": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
     "ub_exchange_copy": (i32, [vp, vp, vp, vp, vp, i32, i64, i64, vp]),
+    "ub_validate_cu_seqlens": (i32, [vp, i32, i32, i64, vp, vp]),
+    "ub_set_checked": (i32, [i32]),
     "ub_ipc_export": (i32, [vp, vp]),
     "ub_ipc_import": (i32, [vp, vp, vp]),
     "ub_ipc_close": (i32, [vp]),

@@ -304,6 +304,19 @@ def exchange_copy(src_tokens, dst_tokens, src_samples, dst_samples, d_tab, B, re
                                  _ptr(d_tab), B, int(rec_bytes), int(srec_bytes), _stream(stream)))
 
 
+# ------------------------------------------------------------------ checked mode
+def set_checked(on: bool):
+    """Validate device cu_seqlens before every unpad / pad / FMHA launch (syncs; tests only)."""
+    check(lib().ub_set_checked(1 if on else 0))
+
+
+def validate_cu_seqlens(cu: torch.Tensor, B: int, max_seqlen: int, T: int, stream=None) -> int:
+    """0 valid, 1 cu[0] != 0, 2 not monotone, 3 a length > max_seqlen, 4 cu[B] > T (syncs)."""
+    flag = torch.full((1,), -1, dtype=torch.int32, device=cu.device)
+    check(lib().ub_validate_cu_seqlens(_ptr(cu), B, max_seqlen, int(T), _ptr(flag), _stream(stream)))
+    return int(flag.item())
+
+
 # ------------------------------------------------------------------ pull exchange (NEXT-3)
 def ipc_export(t: torch.Tensor) -> bytes:
     """Handle (UB_IPC_HANDLE_BYTES) of the device buffer starting at t, for the other ranks."""

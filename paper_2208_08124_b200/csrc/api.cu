@@ -150,6 +150,7 @@ extern "C" ub_status ub_varlen_fmha_fwd(const ub_fmha_params* p, const void* qkv
   if (st != UB_OK) return st;
   UB_REQUIRE(qkv && d_cu && out && lse, UB_ERR_INVALID_ARG, "null pointer");
   if ((st = require_sm100()) != UB_OK) return st;
+  if ((st = checked_cu(d_cu, p->B, p->max_seqlen, p->T, as_stream(stream))) != UB_OK) return st;
   if (p->dtype == UB_BF16) {
     UB_REQUIRE(ws, UB_ERR_INVALID_ARG, "null workspace");
     UB_REQUIRE(((uintptr_t)qkv & 15) == 0 && ((uintptr_t)out & 15) == 0, UB_ERR_INVALID_ARG,
@@ -170,6 +171,7 @@ extern "C" ub_status ub_varlen_fmha_fwd_pad(const ub_fmha_params* p, const void*
   UB_REQUIRE((((uintptr_t)qkv | (uintptr_t)out | (uintptr_t)padded) & 15) == 0, UB_ERR_INVALID_ARG,
              "qkv/out/padded must be 16-B aligned");
   if ((st = require_sm100()) != UB_OK) return st;
+  if ((st = checked_cu(d_cu, p->B, p->max_seqlen, p->T, as_stream(stream))) != UB_OK) return st;
   return fmha_fwd_sm100(*p, qkv, d_cu, out, lse, padded, S, ws, as_stream(stream));
 }
 
@@ -181,6 +183,7 @@ extern "C" ub_status ub_varlen_fmha_bwd(const ub_fmha_params* p, const void* qkv
   if (st != UB_OK) return st;
   UB_REQUIRE(qkv && out && lse && dout && d_cu && dqkv && ws, UB_ERR_INVALID_ARG, "null pointer");
   if ((st = require_sm100()) != UB_OK) return st;
+  if ((st = checked_cu(d_cu, p->B, p->max_seqlen, p->T, as_stream(stream))) != UB_OK) return st;
   if (p->dtype == UB_BF16) {
     UB_REQUIRE(((uintptr_t)qkv & 15) == 0 && ((uintptr_t)dout & 15) == 0 && ((uintptr_t)dqkv & 15) == 0,
                UB_ERR_INVALID_ARG, "qkv/dout/dqkv must be 16-B aligned");

@@ -94,4 +94,8 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// checked mode (checked.cu): validate device cu_seqlens before a launch (sync; tests only)
+bool checked_mode();
+ub_status checked_cu(const int32_t* d_cu, int32_t B, int32_t max_seqlen, int64_t T, cudaStream_t s);
+
 }  // namespace ub

@@ -187,6 +187,7 @@ static ub_status unpad_pad_dispatch(bool pad, const void* src, void* dst, const 
   UB_REQUIRE(T >= 0 && T <= (int64_t)B * S, UB_ERR_CAPACITY, "T=%lld exceeds B*S", (long long)T);
   const uintptr_t al = (uintptr_t)src | (uintptr_t)dst | (uintptr_t)(pad_row ? pad_row : dst);
   cudaStream_t s = as_stream(stream);
+  if (ub_status st = checked_cu(d_cu, B, S, T, s); st != UB_OK) return st;
   if (row_bytes % 16 == 0 && (al & 15) == 0) return launch_span(pad, src, dst, d_cu, pad_row, B, S, T, row_bytes, s);
   if (row_bytes % 4 == 0 && (al & 3) == 0)
     return launch_unpad_pad<uint32_t>(pad, src, dst, d_cu, pad_row, B, S, row_bytes, s);
