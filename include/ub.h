@@ -178,7 +178,10 @@ ub_status ub_dal_bwd(const void* dy, const void* a, const void* res, const void*
  *                     (zero them first); grad_dtype UB_FP32 (16-B fp32 vector reductions)
  *                     or UB_BF16 (bf16x2 vector reductions, the paper's packed-atomic form,
  *                     P:535; less precise for frequent tokens).  Summation order is not
- *                     fixed (atomics): results agree with the oracle within rounding.
+ *                     fixed (atomics): results agree with the oracle within rounding.  The
+ *                     rows of each CTA's most frequent word ids (up to 4, found among its
+ *                     first 128 tokens) are summed in shared memory first and reduced to
+ *                     dW_word once per CTA (skewed vocabularies contend on those rows).
  * ids / pos / seg: int32 [T] device, values in range (not validated on the device, like
  * cu_seqlens); tables bf16 [rows, E]; E a multiple of 8 in [8, 2048] else UB_ERR_UNSUPPORTED;
  * n_type (token-type rows) in [1, 2]; 16-B aligned arrays.  Async on stream. */
