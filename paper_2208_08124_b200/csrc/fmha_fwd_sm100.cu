@@ -515,9 +515,11 @@ static void (*pick_fwd(bool drop, bool big))(CUtensorMap, CUtensorMap, CUtensorM
 
 ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out, float* lse,
                          void* padded, int32_t S_pad, void* ws, cudaStream_t s) {
-  // tuning knob: fraction (x/8) of exp2 pairs on the FMA pipe, 0 or 2 (measured default 2)
-  // measured on config 2: 0 -> 64.5 us, 2 -> 58.4, 3 -> 62.2, 4 -> 68.4 (issue-bound beyond 2/8)
-  static const int poly = env_int("UB_FWD_POLY", 2, 0, 4) >= 2 ? 2 : 0;
+  // fraction (x/8) of exp2 pairs on the FMA pipe, 0 or 2.  Measured on config 2 without
+  // dropout: 0 -> 64.5 us, 2 -> 58.4, 3 -> 62.2, 4 -> 68.4 (issue-bound beyond 2/8); with
+  // dropout the Philox integer work already loads the FMA pipe: 0 -> 92.3 us, 2 -> 99.5.
+  // UB_FWD_POLY = 0 / 2 forces one for both.
+  static const int poly_env = env_int("UB_FWD_POLY", -1, -1, 4);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -526,6 +528,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   const int grid = (int)std::min<int64_t>(ctas, max_items);
   // plan and item table in shared memory, else the global plan decoded per item
   const bool drop = p.p_dropout > 0.f, big = !item_table_fits(p.B, max_items, grid);
+  const int poly = poly_env < 0 ? (drop ? 0 : 2) : (poly_env >= 2 ? 2 : 0);
   void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params) = poly == 2 ? pick_fwd<2>(drop, big) : pick_fwd<0>(drop, big);
   {
     const ub_status sa = smem_attr_once(reinterpret_cast<const void*>(kern), (int)fwd::kSmemBytes);
