@@ -76,7 +76,11 @@ def parse():
                     help="record the per-kernel events on every k-th timed step (event records between kernels "
                          "block their programmatic-dependent-launch overlap)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--reserve-sms", type=int, default=4)
+    ap.add_argument("--reserve-sms", type=int, default=-1,
+                    help="SMs the persistent FMHA grid leaves to the side-stream exchange; -1 = auto (0 at one "
+                         "GPU, where the side stream carries only two small copies; 4 otherwise)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "nccl-forced"],
+                    help="nccl-forced: the self chunk / one-rank all-gather also go through NCCL (UB_COMM_FORCE_NCCL)")
     return ap.parse_args()
 
 
@@ -222,6 +226,40 @@ def rank_lengths(args, world, rank, s):
     return synth.skewed_rank_lengths(world, B, s, args.skew, args.dist)[rank]
 
 
+def rooflines(peaks, clk, ctas, lens_list, fwd_us, bwd_us, padded_fwd=True):
+    """Per-kernel roofline: the kernel's time floor is the max of its tensor
+    floor (strict algorithmic flops: fwd 4 H D sum L^2, bwd 8 H D sum L^2, at the measured
+    BURST bf16 peak -- the timed region is milliseconds long at full clocks), its HBM floor
+    (compulsory bytes: fwd 8256 B/token + the fused pad's padded rows B S H D 2, bwd 16448
+    B/token) and its MUFU floor (H sum L^2 exp2, 16 per clock per SM on the SMs the kernel
+    runs on, at the SM clock sampled during the run).  `bound` names the binding floor,
+    `achieved` / `peak` are in that resource's unit, `frac` = floor / measured time; the
+    tensor fraction is reported beside it whatever binds."""
+    s2 = float(np.mean([float((np.asarray(L, np.float64) ** 2).sum()) for L in lens_list]))
+    T = float(np.mean([float(np.sum(L)) for L in lens_list]))
+    mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
+    mufu_rate = 16.0 * ctas * mhz * 1e6                       # exp2 / s
+    tc_peak = peaks["bf16"] * 1e12
+    bw = peaks["hbm"] * 1e9
+    out = {}
+    for name, us, fl, by in (("fwd", fwd_us, 4.0 * H * D * s2, 8256.0 * T + (B * S * H * D * 2 if padded_fwd else 0)),
+                             ("bwd", bwd_us, 8.0 * H * D * s2, 16448.0 * T)):
+        ex = H * s2
+        floors = {"tensor": fl / tc_peak * 1e6, "hbm": by / bw * 1e6, "alu": ex / mufu_rate * 1e6}
+        bound = max(floors, key=floors.get)
+        t = us * 1e-6
+        ach = {"tensor": (fl / t / 1e12, peaks["bf16"], "TFLOP/s"), "hbm": (by / t / 1e9, peaks["hbm"], "GB/s"),
+               "alu": (ex / t / 1e9, mufu_rate / 1e9, "Gexp2/s")}[bound]
+        out[name] = {"kernel": f"fmha_{name}_kernel", "bound": bound, "achieved": round(ach[0], 1),
+                     "peak": round(ach[1], 1), "unit": ach[2], "frac": round(floors[bound] / us, 4),
+                     "us": round(us, 2), "floors_us": {k: round(v, 2) for k, v in floors.items()},
+                     "tensor_frac": round(fl / t / 1e12 / peaks["bf16"], 4),
+                     "algorithmic": {"flops": fl, "bytes": by, "exp2": ex},
+                     "peak_source": peaks["src"] + " (bf16: burst bf16_tflops; hbm: hbm_gbs; MUFU: 16 ex2/clk/SM "
+                                                   f"(measured, scripts/ubench_ex2.cu) x {ctas} SMs x {mhz:.0f} MHz)"}
+    return out
+
+
 def flops_fwd(L):
     return 4.0 * H * D * float(np.sum(np.asarray(L, np.float64) ** 2))
 
@@ -335,7 +373,11 @@ class Workload:
         # leave SMs free for the side-stream exchange (NCCL + copy kernels) to run
         # concurrently with the persistent FMHA kernels (P:376-381 overlap)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        self.ctas = sms - args.reserve_sms
+        reserve = args.reserve_sms if args.reserve_sms >= 0 else (0 if world == 1 else 4)
+        self.ctas = sms - reserve
+        self.force_nccl = args.exchange == "nccl-forced"
+        if self.force_nccl:
+            self.comm.set_options(force_nccl=True)
 
     def begin(self, n):
         """Side stream, two steps ahead: a1 all-gather of step n's lengths (no host wait)."""
@@ -440,9 +482,11 @@ def run_ours(args, world, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tokens, lens_used = 0, []
     host_step, host_prep, marks = [], [], []
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(wl.main)
     for k in range(args.steps):
         n = args.warmup + k
+        step_ev[k].record(wl.main)
         h0 = time.perf_counter()
         _patch_lse(wl, n)
         m = []
@@ -459,6 +503,7 @@ def run_ours(args, world, rank, local):
         marks.append(np.diff([h0] + m))
         host_step.append(h1 - h0)
         host_prep.append(time.perf_counter() - h1)
+    step_ev[args.steps].record(wl.main)
     wl.main.wait_stream(wl.side)      # steady state: the K steps plus the exchange of the next one
     e1.record(wl.main)
     torch.cuda.synchronize()
@@ -466,9 +511,12 @@ def run_ours(args, world, rank, local):
     clk = clocks.stop()
     for kid in kids:
         ub.api.profile_events(kid)
-    wl.finish(args.warmup + args.steps + PIPE)  # drain the begin still in flight (untimed)
+    last = args.warmup + args.steps + PIPE
+    wl.finish(last)                   # drain the begin still in flight (untimed)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    step_us = [step_ev[k].elapsed_time(step_ev[k + 1]) * 1e3 for k in range(args.steps)]
+    overlap = exchange_overlap(args, wl, world, last, ms / args.steps * 1e3)
     ms_max = all_max(ms, world)
     tok_all = all_sum(tokens, world)
     value = tok_all / (ms_max / 1e3)
@@ -485,15 +533,11 @@ def run_ours(args, world, rank, local):
     fwd_tf = np.mean(f_fwd) / (fwd_us * 1e-6) / 1e12
     bwd_tf = np.mean(f_bwd) / (bwd_us * 1e-6) / 1e12
     mean_T = tokens / args.steps
-    peak_tc = peaks["bf16_sust"] or peaks["bf16"]
+    rl = rooflines(peaks, clk, wl.ctas, [lens_used[i] for i in prof_steps], fwd_us, bwd_us, padded_fwd=True)
     dom = "bwd" if bwd_us >= fwd_us else "fwd"
-    achieved = bwd_tf if dom == "bwd" else fwd_tf
-    traffic = load_traffic().get("fmha_" + dom)
-    roofline = {"kernel": f"fmha_{dom}_kernel", "bound": "tensor", "achieved": round(achieved, 2),
-                "peak": peak_tc, "unit": "TFLOP/s", "frac": round(achieved / peak_tc, 4), "traffic": traffic,
-                "peak_source": peaks["src"] + " bf16_tflops_sustained (kernel timed inside a long step loop)",
-                "flops_convention": "algorithmic, no recompute credit: fwd 4*H*D*sum(L^2), bwd 8*H*D*sum(L^2)",
-                "frac_of_burst_peak": round(achieved / peaks["bf16"], 4)}
+    roofline = dict(rl[dom])
+    roofline["traffic"] = load_traffic().get("fmha_" + dom)
+    roofline["other_kernel"] = rl["fwd" if dom == "bwd" else "bwd"]
     kernels = {"fmha_fwd": {"us": round(fwd_us, 2), "tflops": round(fwd_tf, 1)},
                "fmha_bwd": {"us": round(bwd_us, 2), "tflops": round(bwd_tf, 1)},
                "pad": "fused into fmha_fwd's epilogue (ub_varlen_fmha_fwd_pad); standalone ub_pad under gather",
@@ -529,11 +573,18 @@ def run_ours(args, world, rank, local):
            "data": "synthetic (seeded lengths + N(0,1) bf16 qkv/dO; no dataset)",
            "config": {"workload": f"bert_large_fmha_{args.dist}", "batch_per_gpu": B, "heads": H, "head_dim": D,
                       "max_seqlen": S, "p_dropout": args.p_dropout, "balance": args.balance, "skew": args.skew,
-                      "parallelism": f"dp{world}", "fmha_ctas": wl.ctas, "l2": "rotating 3 input sets; per-step working set > L2",
+                      "parallelism": f"dp{world}", "fmha_ctas": wl.ctas, "exchange": args.exchange, "l2": "rotating 3 input sets; per-step working set > L2",
                       "step": "unpad records + exchange (side stream) | fmha fwd with fused pad + bwd (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
            "tc_util": tc_util,
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
+           "step_us_distribution": {"p10": round(float(np.percentile(step_us, 10)), 2),
+                                    "median": round(float(np.median(step_us)), 2),
+                                    "p90": round(float(np.percentile(step_us, 90)), 2),
+                                    "mean": round(float(np.mean(step_us)), 2), "n": len(step_us),
+                                    "note": "main-stream step boundaries (events); the headline is the whole "
+                                            "K-step region / K"},
+           "exchange_overlap": overlap,
            "main_stream_timeline": timeline, "attn_dropout_0.1": drop01, "length_sweep": sweep, "gather": gather,
            "encoder_attn_sublayer": encoder, "embedding": embedding, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
            "host_us_per_step": dict(zip(["step_setup", "fwd_call", "bwd_call", "pad_call", "unpad_call", "finish_call",
@@ -544,6 +595,50 @@ def run_ours(args, world, rank, local):
     if e2e is not None:
         out["e2e"] = e2e
     return out, wl
+
+
+def exchange_overlap(args, wl, world, last, step_us):
+    """how much of the exchange the overlap hides.
+    compute-only: the same K main-stream steps on batches whose exchange already finished
+    (no side-stream work); isolated: the side stream's per-step work (unpad of the input
+    records, a1-a5) alone, device time between events on that stream, the host plan between
+    its phases included; exposed = overlapped step - compute-only step."""
+    K = args.steps
+    done = [last - i for i in range(N_EX)]              # exchanged batches whose buffers are intact
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for k in range(3):
+        _patch_lse(wl, done[k % N_EX])
+        wl.step(done[k % N_EX])
+    e0.record(wl.main)
+    for k in range(K):
+        n = done[k % N_EX]
+        _patch_lse(wl, n)
+        wl.step(n)
+    e1.record(wl.main)
+    torch.cuda.synchronize()
+    comp = all_max(e0.elapsed_time(e1), world) / K * 1e3
+    # the exchange alone: begin + unpad + finish per step on the side stream, nothing else
+    n0 = last + 1
+    barrier(world)
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wl.begin(n0)
+    wl.side.synchronize()
+    s0.record(wl.side)
+    for k in range(K):
+        wl.begin(n0 + k + 1)
+        wl.finish(n0 + k)
+    s1.record(wl.side)
+    torch.cuda.synchronize()
+    wl.finish(n0 + K)
+    torch.cuda.synchronize()
+    iso = all_max(s0.elapsed_time(s1), world) / K * 1e3
+    return {"overlapped_step_us": round(step_us, 2), "compute_only_step_us": round(comp, 2),
+            "exposed_exchange_us": round(step_us - comp, 2), "isolated_exchange_us": round(iso, 2),
+            "exchange": "nccl" + (" (forced through NCCL at W=1)" if getattr(wl, "force_nccl", False) else ""),
+            "note": "exposed = overlapped - compute-only (negative = within run-to-run noise); isolated = "
+                    "side-stream events around K x (all-gather, unpad, plan, pack, send/recv, unpack)"}
 
 
 def gather_bench(wl, peaks, iters=20):

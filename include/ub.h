@@ -98,8 +98,11 @@ ub_status ub_pad(const void* packed, void* padded, const int32_t* d_cu, int32_t 
  *     O = softmax(scale * Q K^T) V   per sequence b and head h, within the sequence only
  * (unpadded FMHA over packed tokens; no cross-sequence attention, R2), with
  * optional inverted dropout on the probabilities (R4) from the counter-based Philox
- * mask of R5 keyed by (seed, offset): 8-bit decisions, 16 keys per Philox call, p quantised to
- * floor(256 p) / 256 and kept values scaled by the exact inverse keep probability.
+ * mask of R5 keyed by (seed, offset): 8-bit decisions, 16 keys per Philox call.  The drop
+ * rate APPLIED is p_eff = floor(256 p) / 256 (p = 0.1 drops 25/256 = 0.0977 of the
+ * probabilities; ub_dropout_effective_p returns it) and kept values are scaled by the exact
+ * inverse keep probability 1 / (1 - p_eff), so E[P~] = P.  0 < p < 1/256 (p_eff = 0: no
+ * dropout would happen) is rejected with UB_ERR_INVALID_ARG.
  *
  * Work is grouped by length: a device-side plan buckets sequences by their number of
  * 128-token tiles -- the paper's groups (0,128] (128,256] (256,384] (384,512]
@@ -121,7 +124,8 @@ typedef struct {
   int32_t heads;      /* H >= 1 */
   int32_t head_dim;   /* D: 64 for UB_BF16; 1..128 for UB_FP32 */
   float scale;        /* > 0; 1/sqrt(D) in BERT (R1) */
-  float p_dropout;    /* in [0, 1); 0 disables the RNG entirely */
+  float p_dropout;    /* 0 (disables the RNG entirely) or in [1/256, 1); applied as
+                         floor(256 p) / 256 (R5), see ub_dropout_effective_p */
   uint64_t seed;      /* Philox key (R5) */
   uint64_t offset;    /* Philox counter word 3 (low 32 bits used) */
   int32_t dtype;      /* ub_dtype */
@@ -130,6 +134,11 @@ typedef struct {
 } ub_fmha_params;
 
 size_t ub_fmha_workspace_bytes(const ub_fmha_params* prm, int is_bwd);
+
+/* The attention-dropout rate the FMHA kernels apply for a requested p (R5): floor(256 p) / 256
+ * with p taken as float32; 0 for p <= 0.  (The Dropout_Add_LayerNorm kernels use 16-bit
+ * decisions: floor(65536 p) / 65536, see ub_dal_fwd.)  Pure host function. */
+double ub_dropout_effective_p(float p_dropout, int32_t bits);
 
 ub_status ub_varlen_fmha_fwd(const ub_fmha_params* prm, const void* qkv, const int32_t* d_cu,
                              void* out, float* lse, void* ws, void* stream);
@@ -152,9 +161,11 @@ ub_status ub_varlen_fmha_bwd(const ub_fmha_params* prm, const void* qkv, const v
 /* ------------------------------------------------------------------------------------
  * Dropout_Add_LayerNorm (§IV-C-1 kernel fusion; SURVEY §8(f) NEXT-1 piece): one
  * forward kernel, two backward kernels, on packed rows (no padding).
- *   z = res + a * keep / (1 - p),  y = (z - mean) * rstd * gamma + beta,  rstd = 1/sqrt(var + eps)
+ *   z = res + a * keep / (1 - p_eff),  y = (z - mean) * rstd * gamma + beta,  rstd = 1/sqrt(var + eps)
  *   keep: Philox4x32-10, key = seed, counter = (col >> 3, row, 0xDA100000, offset),
- *   16-bit half (col & 1) of word ((col & 7) >> 1) >= floor(p * 65536)   (reading R21)
+ *   16-bit half (col & 1) of word ((col & 7) >> 1) >= thr = floor(p * 65536)   (reading R21);
+ *   p_eff = thr / 65536 is the applied drop rate (ub_dropout_effective_p(p, 16)), so the
+ *   scale is the exact inverse keep probability; 0 < p < 1/65536 is UB_ERR_INVALID_ARG
  * Layouts (device, caller-allocated, 16-B aligned): a, res, y, dy, da, dres [T, E] bf16;
  * gamma, beta [E] bf16; mean, rstd [T] fp32 (written by the forward, read by the backward);
  * dgamma, dbeta [E] fp32.  E a multiple of 8 in [8, 2048] else UB_ERR_UNSUPPORTED;
@@ -338,8 +349,10 @@ ub_status ub_set_checked(int32_t on);
  *   *h_total_tokens (may be NULL) = records this rank receives.  Errors: perm not a
  *   permutation -> SHAPE; negative length -> INVALID_ARG.
  * ub_exchange_pull (device, async on `stream`): d_peer_tokens / d_peer_samples are DEVICE
- *   arrays of W pointers (this rank's own buffers at its own index), each 16-B aligned when
- *   rec_bytes % 16 == 0; d_tab is the pull table in device memory.  One CTA per output
+ *   arrays of W pointers (this rank's own buffers at its own index); 16-B aligned bases take
+ *   the vector path when rec_bytes % 16 == 0, a misaligned peer base is detected per sample
+ *   on the device and copied bytewise (slower, never a fault); d_tab is the pull table in
+ *   device memory.  One CTA per output
  *   sample.  d_ready (may be NULL): DEVICE array of W pointers to the ranks' "buffer
  *   published" flags (IPC-mapped); each CTA first waits, with system-scope acquire, until
  *   the flag of its source rank is >= wait_value, so the host never waits.  Without flags
@@ -371,6 +384,18 @@ ub_status ub_wait_flags(const uint32_t* const* d_flags, int32_t n, uint32_t valu
 ub_status ub_comm_unique_id(void* out_id_128);
 ub_status ub_comm_init(void** out_comm, const void* nccl_unique_id, int32_t W, int32_t rank);
 ub_status ub_comm_destroy(void* comm);
+
+/* Options of a communicator (host, between exchanges).  UB_COMM_FORCE_NCCL: the part of the
+ * exchange a rank keeps for itself, and a one-rank all-gather, also travel through NCCL
+ * (ncclAllGather; ncclSend / ncclRecv to itself inside the step's group) instead of device
+ * copies -- the collective data plane of P:355-359 then runs even on a one-GPU box (tests);
+ * the default (0) copies the self chunk on the device.  Also set by UB_EXCHANGE_FORCE_NCCL=1
+ * at ub_comm_init.  Unknown bits -> UB_ERR_INVALID_ARG. */
+#define UB_COMM_FORCE_NCCL 1
+ub_status ub_comm_set_options(void* comm, int32_t flags);
+/* Number of NCCL calls (all-gathers, sends, receives) this communicator has enqueued so far
+ * (host counter; evidence that the collective data plane ran). */
+ub_status ub_comm_nccl_ops(void* comm, int64_t* out);
 
 /* All-gather of B int32 lengths (P:355 step 1, lengths only): d_my_lengths [B] ->
  * d_all_lengths [W*B] rank-major, on `stream`. */

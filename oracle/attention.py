@@ -176,12 +176,6 @@ def varlen_bwd(qkv, dout, offsets, max_seq_len, scale, p=0.0, seed=0, offset=0, 
     return varlen.unpad(d, lengths)
 
 
-def varlen_delta(out, dout):
-    """Delta_i = sum_d dO_id O_id per (row, head): [H, T] (the backward's row term)."""
-    return np.ascontiguousarray(np.einsum("thd,thd->ht", np.asarray(out, np.float64),
-                                          np.asarray(dout, np.float64)))
-
-
 def default_scale(head_dim: int) -> float:
     """1/sqrt(d_k) (reading R1)."""
     return 1.0 / math.sqrt(head_dim)

@@ -5,13 +5,15 @@ The paper fuses Dropout, Add and LayerNorm of the BERT encoder into one forward 
 two backward kernels (Table table:kernel-fusion: 3 -> 1 and 5 -> 2) and gives no formulas;
 the computation is the textbook one (reading R21 in DESIGN.md):
 
-    z    = res + a * keep / (1 - p)                    (inverted dropout on the sublayer output a)
+    z    = res + a * keep * r                          (inverted dropout on the sublayer output a,
+                                                        r = 1 / (1 - thr / 65536), the exact inverse
+                                                        keep probability of the 16-bit decision)
     mu   = mean_j z_j,   var = mean_j (z_j - mu)^2,    rstd = 1 / sqrt(var + eps)
     y    = (z - mu) * rstd * gamma + beta
 
 backward, with xhat = (z - mu) * rstd and g = dy * gamma:
     dz     = rstd * (g - mean_j g_j - xhat * mean_j (g_j xhat_j))
-    dres   = dz,     da = dz * keep / (1 - p)
+    dres   = dz,     da = dz * keep * r
     dgamma = sum_t dy * xhat,   dbeta = sum_t dy
 
 Dropout mask (reading R21, same Philox4x32-10 as the attention mask R5, own salt):
@@ -33,11 +35,22 @@ from .philox import MASK32, philox4x32_10
 DAL_SALT = 0xDA100000
 
 
+def dal_threshold(p: float) -> int:
+    """thr = floor(p * 65536), p taken as the float32 the API carries (R21)."""
+    return int(np.floor(float(np.float32(p)) * 65536.0))
+
+
+def dal_dropout_scale(p: float) -> float:
+    """r = 1 / (1 - thr / 65536): a 16-bit value is >= thr with probability exactly
+    (65536 - thr) / 65536, so E[keep * r] = 1 (R21; the applied drop rate is thr / 65536)."""
+    return 1.0 / (1.0 - dal_threshold(p) / 65536.0) if p > 0 else 1.0
+
+
 def dal_keep_mask(seed: int, offset: int, T: int, E: int, p: float) -> np.ndarray:
     """keep[t, col] (bool) for rows 0..T-1, columns 0..E-1 -- R21."""
     if p <= 0.0:
         return np.ones((T, E), dtype=bool)
-    thr = int(np.floor(float(np.float32(p)) * 65536.0))      # 16-bit decisions (R21)
+    thr = dal_threshold(p)                                    # 16-bit decisions (R21)
     t = np.arange(T, dtype=np.uint64)[:, None]
     c = np.arange(E, dtype=np.uint64)[None, :]
     tt, cc = np.broadcast_arrays(t, c)
@@ -55,7 +68,7 @@ def dal_fwd(a, res, gamma, beta, p=0.0, eps=1e-12, seed=0, offset=0):
     res = np.asarray(res, np.float64)
     T, E = a.shape
     keep = dal_keep_mask(seed, offset, T, E, p)
-    scale = 1.0 / (1.0 - float(np.float32(p))) if p > 0 else 1.0
+    scale = dal_dropout_scale(p)
     z = res + np.where(keep, a * scale, 0.0)
     mu = z.mean(axis=1)
     var = ((z - mu[:, None]) ** 2).mean(axis=1)
@@ -72,7 +85,7 @@ def dal_bwd(dy, a, res, gamma, p=0.0, eps=1e-12, seed=0, offset=0):
     gamma = np.asarray(gamma, np.float64)
     T, E = a.shape
     keep = dal_keep_mask(seed, offset, T, E, p)
-    scale = 1.0 / (1.0 - float(np.float32(p))) if p > 0 else 1.0
+    scale = dal_dropout_scale(p)
     z = res + np.where(keep, a * scale, 0.0)
     mu = z.mean(axis=1, keepdims=True)
     rstd = 1.0 / np.sqrt(((z - mu) ** 2).mean(axis=1, keepdims=True) + eps)

@@ -6,8 +6,8 @@ tokens[r] ([sum_k L, rec] bytes, sample k at batch_offset[k]) and per-sample
 records samples[r] ([B, srec] bytes).  After the exchange rank d holds the samples
 perm[d*B + 0 .. d*B + B-1] in that order: its packed tokens are the concatenation of
 those samples' token rows, its sample records likewise, and its batch_offset is the
-prefix sum of their lengths.  Pinned by tests/test_oracle_exchange.py (multiset of
-rows preserved, per-sample byte identity, cardinality).
+prefix sum of their lengths.  Pinned by tests/test_oracle_balance.py::test_exchange_simulation (multiset
+of rows preserved, per-sample byte identity, cardinality).
 """
 from __future__ import annotations
 

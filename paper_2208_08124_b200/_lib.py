@@ -13,6 +13,7 @@ STATUS_NAMES = {0: "UB_OK", 1: "UB_ERR_INVALID_ARG", 2: "UB_ERR_INVALID_MASK", 3
                 4: "UB_ERR_SHAPE", 5: "UB_ERR_UNSUPPORTED", 6: "UB_ERR_CUDA", 7: "UB_ERR_NCCL"}
 UB_BF16, UB_FP32 = 0, 1
 UB_IPC_HANDLE_BYTES = 128
+UB_COMM_FORCE_NCCL = 1
 UB_BAL_PAPER, UB_BAL_SNAKE, UB_BAL_EXACT_SMALL, UB_BAL_LPT = 0, 1, 2, 3
 
 # every symbol include/ub.h declares, with (restype, argtypes)
@@ -40,6 +41,7 @@ SIGNATURES = {
     "ub_unpad": (i32, [vp, vp, vp, i32, i32, i64, i64, vp]),
     "ub_pad": (i32, [vp, vp, vp, i32, i32, i64, i64, vp, vp]),
     "ub_fmha_workspace_bytes": (sz, [C.POINTER(FmhaParams), C.c_int]),
+    "ub_dropout_effective_p": (C.c_double, [f32, i32]),
     "ub_varlen_fmha_fwd": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, vp]),
     "ub_varlen_fmha_fwd_pad": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, i32, vp, vp]),
     "ub_varlen_fmha_bwd": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -70,6 +72,8 @@ SIGNATURES = {
     "ub_comm_unique_id": (i32, [vp]),
     "ub_comm_init": (i32, [C.POINTER(vp), vp, i32, i32]),
     "ub_comm_destroy": (i32, [vp]),
+    "ub_comm_set_options": (i32, [vp, i32]),
+    "ub_comm_nccl_ops": (i32, [vp, vp]),
     "ub_allgather_lengths": (i32, [vp, vp, vp, i32, vp]),
     "ub_exchange_workspace_bytes": (sz, [i32, i32, i64, i64, i64]),
     "ub_balance_exchange": (i32, [vp, i32, i32, i32, vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]),

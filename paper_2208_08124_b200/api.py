@@ -60,6 +60,12 @@ def profile_events(kernel_id: int, start=None, stop=None):
                                   stop.cuda_event if stop is not None else None))
 
 
+def dropout_effective_p(p: float, bits: int = 8) -> float:
+    """The drop rate the kernels apply for a requested p: floor(2^bits p) / 2^bits (8-bit
+    attention decisions, R5; 16-bit Dropout_Add_LayerNorm decisions, R21)."""
+    return float(lib().ub_dropout_effective_p(float(p), int(bits)))
+
+
 # ------------------------------------------------------------------ batch_offset
 def cu_seqlens(lengths, max_seqlen: int) -> np.ndarray:
     """Host prefix sum with validation; returns int32 [B+1]."""
@@ -385,6 +391,17 @@ class Comm:
         h = C.c_void_p()
         check(lib().ub_comm_init(C.byref(h), C.cast(raw, C.c_void_p), world, rank))
         self.handle, self.world, self.rank = h, world, rank
+
+    def set_options(self, force_nccl: bool = False):
+        """force_nccl: the self chunk and a one-rank all-gather also go through NCCL
+        (UB_COMM_FORCE_NCCL), so the collective data plane runs on one GPU."""
+        check(lib().ub_comm_set_options(self.handle, 1 if force_nccl else 0))
+
+    def nccl_ops(self) -> int:
+        """NCCL calls (all-gathers, sends, receives) this communicator has enqueued."""
+        v = C.c_int64(0)
+        check(lib().ub_comm_nccl_ops(self.handle, C.byref(v)))
+        return int(v.value)
 
     def allgather_lengths(self, d_lengths: torch.Tensor, out=None, stream=None):
         B = d_lengths.numel()

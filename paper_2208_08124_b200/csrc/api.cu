@@ -74,10 +74,16 @@ extern "C" ub_status ub_profile_events(int32_t kernel_id, void* start_event, voi
   return UB_OK;
 }
 
+extern "C" double ub_dropout_effective_p(float p_dropout, int32_t bits) {
+  if (!(p_dropout > 0.f) || (bits != 8 && bits != 16)) return 0.0;
+  const double levels = bits == 8 ? 256.0 : 65536.0;
+  return std::floor((double)p_dropout * levels) / levels;
+}
+
 extern "C" const char* ub_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" const char* ub_version(void) {
-  return "ubert 0.1 (sm_100a; tcgen05/TMEM/TMA FMHA; NCCL exchange)";
+  return "ubert 0.2 (sm_100a; tcgen05/TMEM/TMA FMHA; NCCL all-gather + send/recv exchange)";
 }
 
 extern "C" ub_status ub_cu_seqlens(const int32_t* h_lengths, int32_t B, int32_t max_seqlen, int32_t* h_cu) {
@@ -123,6 +129,8 @@ static ub_status check_fmha(const ub_fmha_params* p) {
   UB_REQUIRE(p->max_seqlen >= 1, UB_ERR_INVALID_ARG, "max_seqlen < 1");
   UB_REQUIRE(std::isfinite(p->scale) && p->scale > 0.f, UB_ERR_INVALID_ARG, "scale must be > 0");
   UB_REQUIRE(p->p_dropout >= 0.f && p->p_dropout < 1.f, UB_ERR_INVALID_ARG, "p_dropout outside [0,1)");
+  UB_REQUIRE(p->p_dropout == 0.f || ub_dropout_effective_p(p->p_dropout, 8) > 0.0, UB_ERR_INVALID_ARG,
+             "p_dropout %g < 1/256: the 8-bit keep decisions (R5) would drop nothing", (double)p->p_dropout);
   if (p->dtype == UB_BF16) {
     UB_REQUIRE(p->head_dim == 64, UB_ERR_UNSUPPORTED, "bf16 tensor-core path supports head_dim 64 (got %d)", p->head_dim);
   } else if (p->dtype == UB_FP32) {

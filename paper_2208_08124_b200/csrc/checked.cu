@@ -4,7 +4,9 @@
 // caller-provided device flag); with checked mode on (ub_set_checked(1) or UB_CHECKED=1 in
 // the environment) the unpad / pad / FMHA entry points run it first, synchronise the stream
 // and fail with the matching status instead of launching on bad offsets.
+#include <atomic>
 #include <cstdlib>
+#include <mutex>
 
 #include "ub_internal.h"
 
@@ -35,18 +37,26 @@ __global__ void validate_cu_kernel(const int32_t* __restrict__ cu, int32_t B, in
 }
 
 __device__ int32_t g_check_flag;
-static int g_checked = -1;                       // -1: not read from the environment yet
+static std::atomic<int> g_checked{-1};           // -1: not read from the environment yet
+// One device flag serves every checked call: the validate launch, the flag's D2H copy and the
+// stream sync run under this lock, so two checked calls on different streams / host threads
+// cannot read each other's result.
+static std::mutex g_check_mu;
 
 bool checked_mode() {
-  if (g_checked < 0) {
+  int v = g_checked.load(std::memory_order_relaxed);
+  if (v < 0) {
     const char* e = std::getenv("UB_CHECKED");
-    g_checked = (e && e[0] == '1') ? 1 : 0;
+    int want = (e && e[0] == '1') ? 1 : 0;
+    g_checked.compare_exchange_strong(v, want);
+    v = g_checked.load();
   }
-  return g_checked == 1;
+  return v == 1;
 }
 
 ub_status checked_cu(const int32_t* d_cu, int32_t B, int32_t max_seqlen, int64_t T, cudaStream_t s) {
   if (!checked_mode()) return UB_OK;
+  std::lock_guard<std::mutex> lock(g_check_mu);
   int32_t* flag = nullptr;
   UB_CHECK_CUDA(cudaGetSymbolAddress(reinterpret_cast<void**>(&flag), g_check_flag));
   validate_cu_kernel<<<1, 256, 0, s>>>(d_cu, B, max_seqlen, T, flag);
@@ -67,7 +77,7 @@ using namespace ub;
 
 extern "C" ub_status ub_set_checked(int32_t on) {
   clear_error();
-  g_checked = on ? 1 : 0;
+  g_checked.store(on ? 1 : 0);
   return UB_OK;
 }
 

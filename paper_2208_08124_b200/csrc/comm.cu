@@ -36,6 +36,11 @@ struct Comm {
   cudaEvent_t ev_staging = nullptr;
   // UB_EXCHANGE_TRACE=1: host time per finish phase, printed at ub_comm_destroy (dev aid)
   bool trace = false;
+  // UB_COMM_FORCE_NCCL (ub_comm_set_options / UB_EXCHANGE_FORCE_NCCL=1): the self chunk and
+  // the one-rank all-gather go through NCCL too (ncclAllGather, ncclSend/ncclRecv to self)
+  // instead of device copies, so the collective data plane runs on a one-GPU box
+  bool force_nccl = false;
+  int64_t nccl_ops = 0;               // NCCL collectives / point-to-point calls issued (ub_comm_nccl_ops)
   double t_phase[8] = {};
   int64_t n_finish = 0;
 };
@@ -137,6 +142,8 @@ extern "C" ub_status ub_comm_init(void** out_comm, const void* id_128, int32_t W
   Comm* c = new Comm();
   const char* tr = std::getenv("UB_EXCHANGE_TRACE");
   c->trace = tr && tr[0] == '1';
+  const char* fn = std::getenv("UB_EXCHANGE_FORCE_NCCL");
+  c->force_nccl = fn && fn[0] == '1';
   c->W = W;
   c->rank = rank;
   ncclResult_t r = ncclCommInitRank(&c->nccl, W, id, rank);
@@ -171,11 +178,27 @@ extern "C" ub_status ub_comm_destroy(void* comm) {
   return UB_OK;
 }
 
+extern "C" ub_status ub_comm_set_options(void* comm, int32_t flags) {
+  clear_error();
+  UB_REQUIRE(comm, UB_ERR_INVALID_ARG, "null comm");
+  UB_REQUIRE((flags & ~UB_COMM_FORCE_NCCL) == 0, UB_ERR_INVALID_ARG, "unknown option bits 0x%x", flags);
+  static_cast<Comm*>(comm)->force_nccl = (flags & UB_COMM_FORCE_NCCL) != 0;
+  return UB_OK;
+}
+
+extern "C" ub_status ub_comm_nccl_ops(void* comm, int64_t* out) {
+  clear_error();
+  UB_REQUIRE(comm && out, UB_ERR_INVALID_ARG, "null pointer");
+  *out = static_cast<Comm*>(comm)->nccl_ops;
+  return UB_OK;
+}
+
 extern "C" ub_status ub_allgather_lengths(void* comm, const int32_t* d_my, int32_t* d_all, int32_t B, void* stream) {
   clear_error();
   UB_REQUIRE(comm && d_my && d_all && B >= 1, UB_ERR_INVALID_ARG, "bad args");
   Comm* c = static_cast<Comm*>(comm);
   UB_CHECK_NCCL(ncclAllGather(d_my, d_all, (size_t)B, ncclInt32, c->nccl, as_stream(stream)));
+  ++c->nccl_ops;
   return UB_OK;
 }
 
@@ -192,9 +215,13 @@ static ub_status exchange_begin(Comm* c, int32_t slot, int32_t B, const int32_t*
   const size_t n = (size_t)c->W * B;
   int32_t* d_all = static_cast<int32_t*>(ws) + (size_t)slot * n;   // ex_layout: lengths at the front
   // 1. all-gather of lengths (P:355 step 1, lengths only), 2. D2H into the pinned ring
-  // (one rank: the gather is the identity, no collective)
-  if (c->W > 1) UB_CHECK_NCCL(ncclAllGather(d_my_lengths, d_all, (size_t)B, ncclInt32, c->nccl, s));
-  UB_CHECK_CUDA(cudaMemcpyAsync(c->h_all + (size_t)slot * c->W * c->cap_B, c->W > 1 ? d_all : d_my_lengths,
+  // (one rank: the gather is the identity, no collective unless forced)
+  const bool gather = c->W > 1 || c->force_nccl;
+  if (gather) {
+    UB_CHECK_NCCL(ncclAllGather(d_my_lengths, d_all, (size_t)B, ncclInt32, c->nccl, s));
+    ++c->nccl_ops;
+  }
+  UB_CHECK_CUDA(cudaMemcpyAsync(c->h_all + (size_t)slot * c->W * c->cap_B, gather ? d_all : d_my_lengths,
                                 sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
   UB_CHECK_CUDA(cudaEventRecord(c->ev_len[slot], s));
   c->slot_B[slot] = B;
@@ -245,11 +272,17 @@ static ub_status exchange_finish(Comm* c, int32_t slot, int32_t mode, int32_t B,
     return st;
   UB_PHASE();
   // 5. all-to-all-v over NVLink (grouped point-to-point); the chunk a rank keeps is a
-  // device copy, so one rank issues no collective at all
+  // device copy, so one rank issues no collective at all (unless force_nccl: then the self
+  // chunk is an ncclSend/ncclRecv pair to itself inside the same group)
   int64_t so = 0, ro = 0, sso = 0, rso = 0;
   bool any_peer = false;
+  const bool self_nccl = c->force_nccl;
   for (int32_t peer = 0; peer < W; ++peer) {
-    if (peer == me) {
+    if (peer == me && self_nccl) {
+      UB_REQUIRE(send_cnt[me] == recv_cnt[me] && send_scnt[me] == recv_scnt[me], UB_ERR_INVALID_ARG,
+                 "exchange tables disagree on the self chunk");
+      any_peer = any_peer || send_cnt[me] > 0 || send_scnt[me] > 0;
+    } else if (peer == me) {
       UB_REQUIRE(send_cnt[me] == recv_cnt[me] && send_scnt[me] == recv_scnt[me], UB_ERR_INVALID_ARG,
                  "exchange tables disagree on the self chunk");
       if (send_cnt[me] > 0)
@@ -267,7 +300,7 @@ static ub_status exchange_finish(Comm* c, int32_t slot, int32_t mode, int32_t B,
     UB_CHECK_NCCL(ncclGroupStart());
     so = ro = sso = rso = 0;
     for (int32_t peer = 0; peer < W; ++peer) {
-      if (peer != me) {
+      if (peer != me || self_nccl) {
         if (send_cnt[peer] > 0)
           UB_CHECK_NCCL(ncclSend(w.send_tok + so * rec, (size_t)(send_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
         if (recv_cnt[peer] > 0)
@@ -278,6 +311,8 @@ static ub_status exchange_finish(Comm* c, int32_t slot, int32_t mode, int32_t B,
         if (srec > 0 && recv_scnt[peer] > 0)
           UB_CHECK_NCCL(
               ncclRecv(w.recv_smp + rso * srec, (size_t)(recv_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
+        c->nccl_ops += (send_cnt[peer] > 0) + (recv_cnt[peer] > 0) + (srec > 0 && send_scnt[peer] > 0) +
+                       (srec > 0 && recv_scnt[peer] > 0);
       }
       so += send_cnt[peer]; ro += recv_cnt[peer]; sso += send_scnt[peer]; rso += recv_scnt[peer];
     }

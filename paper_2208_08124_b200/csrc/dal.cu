@@ -26,7 +26,7 @@ constexpr uint32_t kSalt = 0xDA100000u;
 struct Params {
   int64_t T;
   int32_t E, V;                               // V = E / 8 vectors per row
-  float eps, rp;                              // rp = 1 / (1 - p)
+  float eps, rp;                              // rp = 1 / (1 - thr / 65536)
   uint32_t thr, k0, k1, off;
 };
 
@@ -225,6 +225,13 @@ static int grid_for(int64_t T, int per_sm) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
 }
 constexpr int kFwdPerSm = 3, kBwdPerSm = 2;   // resident CTAs per SM (launch bounds)
+// The backward workspace holds one partial per CTA.  Its size must not depend on whichever
+// device is current when it is queried: it is sized for the largest grid any device can get
+// (kMaxSms SMs), and the launch never exceeds it.
+constexpr int kMaxSms = 256;
+static int64_t max_bwd_grid(int64_t T) {
+  return std::max<int64_t>(1, std::min<int64_t>((T + kWarps - 1) / kWarps, (int64_t)kMaxSms * kBwdPerSm));
+}
 
 static Params make_params(int64_t T, int32_t E, float p, float eps, uint64_t seed, uint64_t offset) {
   Params q{};
@@ -232,8 +239,8 @@ static Params make_params(int64_t T, int32_t E, float p, float eps, uint64_t see
   q.E = E;
   q.V = E / 8;
   q.eps = eps;
-  q.rp = p > 0.f ? 1.f / (1.f - p) : 1.f;
-  q.thr = p > 0.f ? (uint32_t)floor((double)p * 65536.0) : 0u;
+  q.thr = p > 0.f ? (uint32_t)floor((double)p * 65536.0) : 0u;        // R21: 16-bit decisions
+  q.rp = p > 0.f ? (float)(1.0 / (1.0 - q.thr / 65536.0)) : 1.f;        // exact inverse keep probability
   q.k0 = (uint32_t)(seed & 0xFFFFFFFFull);
   q.k1 = (uint32_t)(seed >> 32);
   q.off = (uint32_t)(offset & 0xFFFFFFFFull);
@@ -266,6 +273,8 @@ static ub_status check_args(int64_t T, int32_t E, float p, float eps) {
   UB_REQUIRE(E >= 8 && E % 8 == 0 && E <= 32 * kMaxVec * 8, UB_ERR_UNSUPPORTED,
              "E = %d: need a multiple of 8 in [8, 2048]", E);
   UB_REQUIRE(p >= 0.f && p < 1.f, UB_ERR_INVALID_ARG, "p_dropout %f not in [0, 1)", (double)p);
+  UB_REQUIRE(p == 0.f || floor((double)p * 65536.0) >= 1.0, UB_ERR_INVALID_ARG,
+             "p_dropout %g < 1/65536: the 16-bit keep decisions (R21) would drop nothing", (double)p);
   UB_REQUIRE(eps > 0.f, UB_ERR_INVALID_ARG, "eps <= 0");
   return UB_OK;
 }
@@ -299,7 +308,7 @@ extern "C" ub_status ub_dal_fwd(const void* a, const void* res, const void* gamm
 }
 
 extern "C" size_t ub_dal_bwd_workspace_bytes(int64_t T, int32_t E) {
-  return (size_t)dal::grid_for(T, dal::kBwdPerSm) * 2 * (size_t)(E > 0 ? E : 0) * sizeof(float);
+  return (size_t)dal::max_bwd_grid(T) * 2 * (size_t)(E > 0 ? E : 0) * sizeof(float);
 }
 
 extern "C" ub_status ub_dal_bwd(const void* dy, const void* a, const void* res, const void* gamma, const float* mean,
@@ -314,7 +323,7 @@ extern "C" ub_status ub_dal_bwd(const void* dy, const void* a, const void* res, 
                  0,
              UB_ERR_INVALID_ARG, "bf16 arrays must be 16-B aligned");
   const dal::Params q = dal::make_params(T, E, p_dropout, 1.f, seed, offset);
-  const int grid = dal::grid_for(T, dal::kBwdPerSm);
+  const int grid = (int)std::min<int64_t>(dal::grid_for(T, dal::kBwdPerSm), dal::max_bwd_grid(T));
   const bool drop = p_dropout > 0.f;
   cudaStream_t s = as_stream(stream);
   float* part = static_cast<float*>(ws);

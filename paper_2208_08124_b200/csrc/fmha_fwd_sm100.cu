@@ -481,7 +481,26 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       epilogue(opk);
     }
   } else {
-    regs_dec<88>();                // warps 10-11: idle
+    regs_dec<88>();                // warps 10-11: otherwise idle
+    if (warp == 10 && prm.padded) {
+      // fused pad of EMPTY sequences (L = 0 has no work item, so no epilogue zeroes its
+      // padded block): CTA c zero-fills [b, 0:S, h, :] of b = c, c + G, ... with TMA stores
+      // of the zero block, one (head, 32-row block) per lane -- the ub_pad result
+      const int32_t nblk = prm.S_pad / 32;
+      bool issued = false;
+      for (int32_t b = (int32_t)blockIdx.x; b < prm.B; b += (int32_t)gridDim.x) {
+        if (prm.cu[b + 1] - prm.cu[b] != 0) continue;
+        for (int32_t w = (int32_t)lane; w < H * nblk; w += 32) {
+          const int32_t h = w / nblk, blk = w - h * nblk;
+          tma_store_2d(&tmap_pad, sm.zeros, h * kD, b * prm.S_pad + blk * 32);
+          issued = true;
+        }
+      }
+      if (issued) {
+        bulk_commit_group();
+        bulk_wait_group0();
+      }
+    }
   }
 
   if (warp < 8 && lane == 0) bulk_wait_group0();        // output stores complete before exit

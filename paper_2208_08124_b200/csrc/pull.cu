@@ -48,12 +48,20 @@ __global__ void __launch_bounds__(256) exchange_pull_kernel(const uint8_t* const
     if (threadIdx.x == 0) spin_until_ge(ready[src], wait_value);
     __syncthreads();
   }
-  const Vec* s = reinterpret_cast<const Vec*>(peer_tok[src] + src_tok * rec);
-  Vec* d = reinterpret_cast<Vec*>(dt + dst_tok * rec);
-  const int64_t nv = len * rec / (int64_t)sizeof(Vec);
-  // gridDim.y CTAs share a sample (large records): interleaved 256-vector blocks
-  for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.y * blockDim.x)
-    d[i] = s[i];
+  const uint8_t* sb = peer_tok[src] + src_tok * rec;
+  uint8_t* db = dt + dst_tok * rec;
+  const int64_t stride = (int64_t)gridDim.y * blockDim.x;
+  if (((uintptr_t)sb & (sizeof(Vec) - 1)) == 0) {
+    const Vec* s = reinterpret_cast<const Vec*>(sb);
+    Vec* d = reinterpret_cast<Vec*>(db);
+    const int64_t nv = len * rec / (int64_t)sizeof(Vec);
+    // gridDim.y CTAs share a sample (large records): interleaved 256-vector blocks
+    for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < nv; i += stride) d[i] = s[i];
+  } else {
+    // a peer base the caller mapped at an offset not aligned to the vector width (the host
+    // cannot see the device pointer table): byte copy for this sample instead of a fault
+    for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < len * rec; i += stride) db[i] = sb[i];
+  }
   if (srec > 0 && blockIdx.y == 0) {
     const uint8_t* ss = peer_smp[src] + tab[4 * B + e] * srec;
     uint8_t* dd = ds + tab[5 * B + e] * srec;
@@ -178,7 +186,8 @@ extern "C" ub_status ub_exchange_pull(const void* const* d_peer_tokens, const vo
   auto* ps = reinterpret_cast<const uint8_t* const*>(d_peer_samples);
   auto* dt = static_cast<uint8_t*>(dst_tokens);
   auto* ds = static_cast<uint8_t*>(dst_samples);
-  // peer buffers are the callers' (16-B aligned allocations); the vector width follows rec.
+  // the vector width follows rec and dst; a peer base that is not aligned to it is detected
+  // per sample on the device (byte-copy path), since the pointer table is device memory.
   // Large records (a hidden row per token): 16 CTAs per sample, else one.
   const dim3 grid(B, rec_bytes >= 256 ? 16 : 1);
   if (rec_bytes % 16 == 0 && ((uintptr_t)dst_tokens & 15) == 0)

@@ -39,6 +39,17 @@ def test_exports_every_declared_symbol(ub):
     assert "sm_100a" in L.ub_version().decode()
 
 
+def test_dropout_effective_p(ub):
+    """The applied drop rates (R5 8-bit, R21 16-bit) agree with the oracle's thresholds."""
+    from oracle import dal as odal
+    from oracle import philox
+    from paper_2208_08124_b200 import api
+    for p in (0.0, 0.1, 0.25, 0.5, 1.0 / 3.0, 0.9):
+        assert api.dropout_effective_p(p, 8) == philox.dropout_threshold(p) / 256.0
+        assert api.dropout_effective_p(p, 16) == (odal.dal_threshold(p) / 65536.0 if p > 0 else 0.0)
+    assert api.dropout_effective_p(0.001, 8) == 0.0      # rejected by the FMHA entry points
+
+
 def test_cu_seqlens_and_errors(ub, golden):
     from paper_2208_08124_b200 import api
     for ex in golden["spec_worked_examples"]["batch_offset"]:

@@ -80,6 +80,32 @@ def test_bf16_fwd_deterministic_and_single_sequence(ub):
     assert torch.equal(d[:, 2], dout.float())                         # dV = dO
 
 
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_bf16_config2_full_batch_every_sequence(ub, p):
+    """BASELINE config 2 exactly as bench.py runs it (56 x mlperf_like_v0 lengths up to 512,
+    16 heads x 64, bf16, persistent grid), at p = 0 and at BERT-large's attention dropout
+    p = 0.1: EVERY sequence's O, LSE, dQ, dK, dV element by element against the fp64 oracle
+    (per sequence, absolute dropout coordinates), under the BASELINE tolerance."""
+    L = synth.gen_lengths("mlperf_like_v0", 56, 0)
+    seed = 0x2208
+    lengths, off, qkv, dout, o, lse, d, scale = _run(ub, L, 16, 64, torch.bfloat16, p=p, seed=seed, max_seqlen=512)
+    ref = oracle_seq_slice(qkv, dout, off, range(len(L)), scale, p=p, seed=seed, offset=0)
+    worst = {}
+    for b in range(len(L)):
+        s, e = int(off[b]), int(off[b + 1])
+        O, LSE, dq = ref[b]
+        worst.setdefault("O", []).append(assert_close(o[s:e].float().numpy(), O, f"O seq{b} L={e - s}"))
+        assert_close(lse[:, s:e].numpy(), LSE, f"LSE seq{b}", TOL_LSE, 1.0)
+        for i, name in enumerate("qkv"):
+            worst.setdefault(name, []).append(assert_close(d[s:e, i].float().numpy(), dq[:, i],
+                                                           f"d{name} seq{b} L={e - s}"))
+    # the whole batch as one tensor, too (rel-L2 over all 56 sequences)
+    O_all = np.concatenate([ref[b][0] for b in range(len(L))])
+    D_all = np.concatenate([ref[b][2] for b in range(len(L))])
+    assert_close(o.float().numpy(), O_all, "O batch")
+    assert_close(d.float().numpy(), D_all, "dqkv batch")
+
+
 @pytest.mark.parametrize("dist,seed", [("mlperf_like_v0", 0), ("uniform", 1), ("bimodal", 2)])
 def test_bf16_bert_large_full_size_sampled(ub, dist, seed):
     """BASELINE config 2 / 5 at full size (56 x up to 512, 16 heads x 64) in the launch
@@ -108,22 +134,33 @@ def test_bf16_bert_large_full_size_sampled(ub, dist, seed):
 
 
 def test_bf16_dropout_mask_matches_oracle(ub):
-    """With V = identity-like one-hot rows, O exposes P~ directly: the GPU's dropout
-    pattern must equal the oracle's Philox mask (R5) bitwise (kept <=> nonzero)."""
-    L, H, D = 64, 2, 64
-    lengths, off, qkv, dout = make_batch([L], H, D)
+    """The dropout mask of BOTH kernels equals the oracle's Philox mask (R5) bitwise, at all
+    16 heads and at several packed-row offsets (the counter words t, h of R5):
+      forward  -- V rows one-hot (v_j = e_j): O[i, d=j] = P~[i, j], kept <=> O != 0;
+      backward -- dO rows one-hot (dO_i = e_i): dV[j, d=i] = P~[i, j], kept <=> dV != 0."""
+    Ls, H, D = [64, 40, 64, 17], 16, 64
+    lengths, off, qkv, dout = make_batch(Ls, H, D)
     qkv[:, 2] = 0
-    for j in range(L):
-        qkv[j, 2, :, j] = 1.0                       # v_j = e_j -> O[i, d=j] = P~[i, j]
+    dout[:] = 0
+    for b, L in enumerate(Ls):
+        s = int(off[b])
+        for j in range(L):
+            qkv[s + j, 2, :, j] = 1.0                   # v_j = e_j
+            dout[s + j, :, j] = 1.0                     # dO_j = e_j
     qd = qkv.cuda()
     cu = torch.tensor(off.astype(np.int32)).cuda()
-    o, _ = ub.varlen_fmha_fwd(qd, cu, 512, None, 0.3, 1234, 5)
+    p, seed, offs = 0.3, 1234, 5
+    o, lse = ub.varlen_fmha_fwd(qd, cu, 512, None, p, seed, offs)
+    d = ub.varlen_fmha_bwd(qd, o, lse, dout.cuda(), cu, 512, None, p, seed, offs)
     torch.cuda.synchronize()
+    o, dv = o.float().cpu().numpy(), d[:, 2].float().cpu().numpy()
     from oracle import philox
-    for h in range(H):
-        keep = philox.keep_mask_block(1234, 5, 0, L, h, 0.3)
-        got = (o[:, h, :L].float().cpu().numpy() != 0)
-        assert np.array_equal(got, keep), h
+    for b, L in enumerate(Ls):
+        s = int(off[b])
+        for h in range(H):
+            keep = philox.keep_mask_block(seed, offs, s, L, h, p)          # [query i, key j]
+            assert np.array_equal(o[s:s + L, h, :L] != 0, keep), (b, h)
+            assert np.array_equal((dv[s:s + L, h, :L] != 0).T, keep), (b, h)
 
 
 def test_invalid_arguments(ub):
@@ -137,6 +174,9 @@ def test_invalid_arguments(ub):
     cu = torch.tensor(off.astype(np.int32)).cuda()
     with pytest.raises(UbError) as e:
         ub.varlen_fmha_fwd(qkv.cuda(), cu, 512, p_dropout=1.0)
+    assert e.value.status == 1
+    with pytest.raises(UbError) as e:                     # p < 1/256: R5's 8-bit decisions drop nothing
+        ub.varlen_fmha_fwd(qkv.cuda(), cu, 512, p_dropout=0.003)
     assert e.value.status == 1
 
 
@@ -158,7 +198,7 @@ def test_bwd_repeatable_across_changing_batches(ub):
 
 
 def test_bf16_more_sequences_than_smem_plan(ub):
-    """B > kPlanCap (1024): the kernels fall back to the separate plan kernel and the
+    """B > kPlanCap (512): the kernels fall back to the separate plan kernel and the
     global-memory work decode; results must match the oracle on sampled sequences."""
     rng = np.random.default_rng(3)
     L = rng.integers(1, 60, size=1100)
@@ -197,9 +237,11 @@ def test_item_table_overflow_same_results(ub):
 def test_fwd_with_fused_pad(ub, p):
     """ub_varlen_fmha_fwd_pad (a7 + a9): out / lse identical to the plain forward, padded
     identical (bitwise) to ub_pad of out -- zeros past each length, including whole padded
-    tiles and sequences of one token."""
-    L = np.array([1, 31, 32, 33, 127, 128, 129, 300, 512, 64], np.int32)
-    lengths, off, qkv, dout = make_batch(L, 4, 64)
+    tiles, sequences of one token and EMPTY sequences (no work item: zero-filled by the
+    kernel's otherwise idle warp)."""
+    L = np.array([1, 31, 32, 33, 127, 128, 129, 300, 0, 512, 64, 0], np.int32)   # incl. empty sequences
+    off = np.concatenate([[0], np.cumsum(L)]).astype(np.int64)      # (the oracle rejects L = 0, R8)
+    qkv = synth.gen_normal((int(off[-1]), 3, 4, 64), 1000)
     qd = qkv.cuda()
     cu = torch.tensor(off.astype(np.int32)).cuda()
     S = 512

@@ -110,14 +110,18 @@ def test_exchange_pack_transport_unpack_virtual_ranks(ub, W, rec, srec, mode):
             assert obal.imbalance(plan["rank_tokens"]) <= 0.05   # BASELINE gate (B = 56)
 
 
-def test_nccl_balance_exchange_single_rank(ub):
-    """The full NCCL path (all-gather, plan, pack, grouped send/recv, unpack, cu H2D) at
-    W=1 on the one GPU this run has: the output is the paper's sorted order."""
+@pytest.mark.parametrize("force_nccl", [False, True])
+def test_nccl_balance_exchange_single_rank(ub, force_nccl):
+    """The full exchange (all-gather, plan, pack, grouped send/recv, unpack, cu H2D) at W=1
+    on the one GPU this run has: the output is the paper's sorted order.  force_nccl routes
+    the one-rank all-gather and the self chunk through ncclAllGather / ncclSend+ncclRecv
+    (UB_COMM_FORCE_NCCL): the collective data plane itself moves the bytes."""
     B, rec, srec = 56, 16, 4
     lens = synth.gen_lengths("mlperf_like_v0", B, 5)
     toks = synth.gen_bytes(int(lens.sum()) * rec, 91).reshape(-1, rec)
     smps = synth.gen_bytes(B * srec, 92).reshape(B, srec)
     comm = ub.Comm(1, 0)
+    comm.set_options(force_nccl=force_nccl)
     side = torch.cuda.Stream()
     ot, os_, ocu, T, perm = comm.balance_exchange(torch.from_numpy(lens).cuda(), torch.from_numpy(toks).cuda(),
                                                   torch.from_numpy(smps).cuda(), int(lens.sum()), 512, stream=side)
@@ -129,15 +133,20 @@ def test_nccl_balance_exchange_single_rank(ub):
     assert np.array_equal(ot[:T].cpu().numpy(), exp["tokens"])
     assert np.array_equal(os_.cpu().numpy(), exp["samples"])
     assert np.array_equal(ocu.cpu().numpy(), exp["cu"])
+    # all-gather + token send + token recv + sample send + sample recv when forced; none otherwise
+    assert comm.nccl_ops() == (5 if force_nccl else 0)
     comm.close()
 
 
 @pytest.mark.gpu
-def test_nccl_exchange_two_phase_pipelined(ub):
+@pytest.mark.parametrize("force_nccl", [False, True])
+def test_nccl_exchange_two_phase_pipelined(ub, force_nccl):
     """ub_exchange_begin / ub_exchange_finish with several batches in flight (the bench's
-    pipeline: begin n+2 before finish n+1) give what the oracle's exchange gives per batch."""
+    pipeline: begin n+2 before finish n+1) give what the oracle's exchange gives per batch,
+    with the copies or (force_nccl) NCCL itself moving the data."""
     B, rec, srec = 56, 16, 4
     comm = ub.Comm(1, 0)
+    comm.set_options(force_nccl=force_nccl)
     side = torch.cuda.Stream()
     batches = []
     for k in range(6):
@@ -168,6 +177,7 @@ def test_nccl_exchange_two_phase_pipelined(ub):
         assert np.array_equal(ot[:T].cpu().numpy(), exp["tokens"])
         assert np.array_equal(os_.cpu().numpy(), exp["samples"])
         assert np.array_equal(ocu.cpu().numpy(), exp["cu"])
+    assert comm.nccl_ops() == (5 * len(batches) if force_nccl else 0)
     # misuse: finish without a begin, begin on a busy slot, slot out of range
     d = batches[0]
     with pytest.raises(ub.UbError):

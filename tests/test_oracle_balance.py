@@ -125,6 +125,9 @@ def test_exchange_simulation():
     assert all_rows == got_rows                                            # multiset preserved
     for d in range(W):
         assert out[d]["cu"][-1] == plan["rank_tokens"][d]
+        # the rank's post-exchange batch_offset from the plan alone equals the offsets of the
+        # records the simulation actually moved
+        assert np.array_equal(balance.cu_seqlens_for_rank(lens.reshape(-1), plan["perm"], W, B, d), out[d]["cu"])
         for k in range(B):
             g = int(plan["perm"][d * B + k]); s, kk = divmod(g, B)
             a0, a1 = out[d]["cu"][k], out[d]["cu"][k + 1]

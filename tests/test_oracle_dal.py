@@ -17,7 +17,7 @@ def _torch_ref(a, res, gamma, beta, dy, keep, p, eps):
     rt = torch.tensor(res, requires_grad=True)
     gt = torch.tensor(gamma, requires_grad=True)
     bt = torch.tensor(beta, requires_grad=True)
-    m = torch.tensor(keep, dtype=torch.float64) / (1.0 - float(np.float32(p)) if p > 0 else 1.0)
+    m = torch.tensor(keep, dtype=torch.float64) * dal.dal_dropout_scale(p)   # scale pinned below
     y = torch.nn.functional.layer_norm(rt + at * m, (a.shape[1],), gt, bt, eps)
     y.backward(torch.tensor(dy))
     return y.detach().numpy(), at.grad.numpy(), rt.grad.numpy(), gt.grad.numpy(), bt.grad.numpy()
@@ -65,3 +65,17 @@ def test_invariants_and_mask():
     # dropped entries of a do not reach y: da is exactly zero there
     keep = dal.dal_keep_mask(7, 0, 50, 64, 0.1)
     assert np.all(da[~keep] == 0.0)
+
+
+def test_scale_is_exact_inverse_keep_probability():
+    """R21: a kept value is scaled by 1 / P(keep).  P(keep) by brute force over the whole
+    16-bit space (r >= thr for r = 0..65535), so E[keep * r] = 1 exactly, for p on and off
+    the 1/65536 grid; and the empirical keep fraction of a large mask matches it."""
+    r16 = np.arange(65536)
+    for p in (0.1, 0.25, 0.5, 1.0 / 3.0, 0.9, 3.0 / 65536):
+        pk = np.count_nonzero(r16 >= dal.dal_threshold(p)) / 65536.0
+        assert abs(dal.dal_dropout_scale(p) * pk - 1.0) < 1e-15, p
+    assert dal.dal_dropout_scale(0.0) == 1.0
+    k = dal.dal_keep_mask(2, 0, 512, 1024, 0.1)
+    pk = np.count_nonzero(r16 >= dal.dal_threshold(0.1)) / 65536.0
+    assert abs(k.mean() - pk) < 5 * np.sqrt(pk * (1 - pk) / k.size)

@@ -38,7 +38,7 @@ def test_matches_torch_autograd_composition():
         ctx.append(o.transpose(0, 1).reshape(e - s, hid))
     a = torch.cat(ctx) @ t["wo"].T + t["bo"]
     keep = torch.tensor(odal.dal_keep_mask(seed, 0, T, hid, p_hidden), dtype=torch.float64)
-    ty = torch.nn.functional.layer_norm(t["x"] + a * keep / (1 - float(np.float32(p_hidden))), (hid,), t["g"], t["b"], eps)
+    ty = torch.nn.functional.layer_norm(t["x"] + a * keep * odal.dal_dropout_scale(p_hidden), (hid,), t["g"], t["b"], eps)
     ty.backward(torch.tensor(dy))
     assert np.allclose(y, ty.detach().numpy(), atol=1e-10)
     for name, key in (("dx", "x"), ("dw_qkv", "wq"), ("db_qkv", "bq"), ("dw_o", "wo"), ("db_o", "bo"),
