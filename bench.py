@@ -67,7 +67,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--dist", default="mlperf_like_v0", choices=list(synth.DISTRIBUTIONS))
     ap.add_argument("--p-dropout", type=float, default=0.0)
-    ap.add_argument("--balance", default="paper", choices=["paper", "snake", "lpt"])
+    ap.add_argument("--balance", default="paper",
+                    choices=["paper", "snake", "lpt", "stay", "paper+locality", "snake+locality", "lpt+locality"])
     ap.add_argument("--skew", default="iid", choices=["iid", "sorted-block"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -76,9 +77,9 @@ def parse():
                     help="record the per-kernel events on every k-th timed step (event records between kernels "
                          "block their programmatic-dependent-launch overlap)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--reserve-sms", type=int, default=-1,
-                    help="SMs the persistent FMHA grid leaves to the side-stream exchange; -1 = auto (0 at one "
-                         "GPU, where the side stream carries only two small copies; 4 otherwise)")
+    ap.add_argument("--reserve-sms", type=int, default=4,
+                    help="SMs the persistent FMHA grid leaves to the side-stream exchange (r02c: 0 left the "
+                         "side-stream copies no SM while the FMHA kernels ran: 280 vs 214 us per step)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "nccl-forced"],
                     help="nccl-forced: the self chunk / one-rank all-gather also go through NCCL (UB_COMM_FORCE_NCCL)")
     return ap.parse_args()
@@ -373,8 +374,7 @@ class Workload:
         # leave SMs free for the side-stream exchange (NCCL + copy kernels) to run
         # concurrently with the persistent FMHA kernels (P:376-381 overlap)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        reserve = args.reserve_sms if args.reserve_sms >= 0 else (0 if world == 1 else 4)
-        self.ctas = sms - reserve
+        self.ctas = sms - args.reserve_sms
         self.force_nccl = args.exchange == "nccl-forced"
         if self.force_nccl:
             self.comm.set_options(force_nccl=True)
@@ -894,18 +894,27 @@ def planned_imbalance(args, steps=20):
     from paper_2208_08124_b200 import api
     out = {}
     for W in (2, 4, 8):
-        rec = {"before": [], "paper": [], "snake": [], "lpt": []}
+        rec = {"before": [], "paper": [], "snake": [], "lpt": [], "stay": []}
+        moved = {m: [] for m in ("paper", "paper+locality", "lpt", "lpt+locality", "stay")}
         for skew in ("iid", "sorted-block"):
             for k in range(steps):
                 a = synth.skewed_rank_lengths(W, B, 1000 + k, skew, args.dist)
                 tok = a.sum(axis=1).astype(np.float64)
                 rec["before"].append(tok.max() / tok.mean() - 1)
-                for mode in ("paper", "snake", "lpt"):
+                for mode in ("paper", "snake", "lpt", "stay"):
                     rt = api.balance_plan(a.reshape(-1), W, B, S, mode)["rank_tokens"].astype(np.float64)
                     rec[mode].append(rt.max() / rt.mean() - 1)
+                if skew == "iid":
+                    flat = a.reshape(-1)
+                    for mode in moved:
+                        perm = api.balance_plan(flat, W, B, S, mode)["perm"]
+                        kept = sum(int(flat[g]) for r in range(W) for g in perm[r * B:(r + 1) * B] if g // B == r)
+                        moved[mode].append(1.0 - kept / float(flat.sum()))
         out[f"w{W}"] = {k: {"mean": round(float(np.mean(v)), 5), "max": round(float(np.max(v)), 5)}
                         for k, v in rec.items()}
-    out["note"] = f"{steps} steps x (iid, sorted-block) skews, {args.dist}, B={B}/rank"
+        out[f"w{W}"]["moved_token_fraction"] = {k: round(float(np.mean(v)), 4) for k, v in moved.items()}
+    out["note"] = (f"{steps} steps x (iid, sorted-block) skews, {args.dist}, B={B}/rank; moved_token_fraction: "
+                   "share of tokens the all-to-all-v moves (iid skew), without / with the locality relabeling (R24)")
     return out
 
 

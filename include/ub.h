@@ -264,6 +264,13 @@ ub_status ub_encoder_attn_bwd(const ub_encoder_params* prm, const void* x, const
  *     paper's plan when that has a strictly smaller maximum); samples on a rank listed by
  *     (length asc, id asc).  A beyond-the-paper variant of P:359 (
  *     steps in DESIGN.md and oracle/balance.py balance_lpt).
+ *   UB_BAL_STAY (reading R25, NEXT-2 locality-aware): every rank starts with its own samples
+ *     and UB_BAL_LPT's swap refinement balances the tokens, so only the swapped samples move
+ *     (a few per cent of the tokens instead of (W-1)/W); ranks list samples by (length, id).
+ *   | UB_BAL_LOCALITY (flag, OR-ed into any mode; reading R24, NEXT-2 beyond the paper): the
+ *     mode's W groups are then handed to the ranks so that the most tokens stay on their
+ *     source rank (group i -> rank sigma[i] maximising the kept tokens; exact, ties ->
+ *     lexicographically smallest sigma; see ub_balance_relabel).  Loads are unchanged.
  * Outputs (host, caller-allocated):
  *   h_perm [W*B]         perm[r*B + k] = global id of the k-th sample placed on rank r
  *   h_rank_tokens [W]    tokens per rank after the exchange (may be NULL)
@@ -271,11 +278,22 @@ ub_status ub_encoder_attn_bwd(const ub_encoder_params* prm, const void* x, const
  *   h_send_tokens [W*W]  tokens moving src -> dst (may be NULL)
  * Errors: W < 1, B < 1, a length < 1 -> INVALID_ARG; length > max_seqlen -> CAPACITY.
  */
-typedef enum { UB_BAL_PAPER = 0, UB_BAL_SNAKE = 1, UB_BAL_EXACT_SMALL = 2, UB_BAL_LPT = 3 } ub_bal_mode;
+typedef enum { UB_BAL_PAPER = 0, UB_BAL_SNAKE = 1, UB_BAL_EXACT_SMALL = 2, UB_BAL_LPT = 3, UB_BAL_STAY = 4 } ub_bal_mode;
+#define UB_BAL_LOCALITY 0x100
 
 ub_status ub_balance_plan(const int32_t* h_all_lengths, int32_t W, int32_t B, int32_t max_seqlen,
                           int32_t mode, int32_t* h_perm, int64_t* h_rank_tokens,
                           int32_t* h_send_samples, int64_t* h_send_tokens);
+
+/* Locality relabeling of a plan (reading R24): the W groups of h_perm
+ * (rank r's block perm[r*B .. r*B+B-1]) keep their contents and order but move to the ranks
+ * sigma[0..W-1] that maximise the tokens staying home, sum_i M[i][sigma[i]] with M[i][r] =
+ * tokens of group i whose source rank (g / B) is r -- an assignment problem solved exactly
+ * by dynamic programming over rank subsets; ties -> lexicographically smallest sigma.
+ * h_perm is rewritten in place; h_kept_before / h_kept_after (may be NULL) = kept tokens.
+ * W <= 20 (2^W states) else UB_ERR_UNSUPPORTED; a perm that is not a permutation -> SHAPE. */
+ub_status ub_balance_relabel(const int32_t* h_all_lengths, int32_t W, int32_t B, int32_t* h_perm,
+                             int64_t* h_kept_before, int64_t* h_kept_after);
 
 /* Cost-aware balancing (NEXT-2): UB_BAL_LPT's steps on the integer per-sample cost
  * alpha*L + beta*L^2 -- the linear layers grow with L, attention with L^2 (Eq. 1).

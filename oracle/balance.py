@@ -15,6 +15,10 @@ enumerators, with the canonical tie-break "lexicographically smallest perm vecto
 Beyond the paper (reading R20, NEXT-2): cardinality-constrained LPT with swap refinement
 on an integer cost alpha*L + beta*L^2, floored by the paper's plan.
 
+Beyond the paper (reading R24, NEXT-2): relabel_locality -- the plan's W groups handed to the
+ranks so that the most tokens stay home (exhaustive over the W! labelings); (reading R25)
+balance_stay -- start from "every rank keeps its samples" and balance by R20's swaps.
+
 Outputs use the library's layout: perm[r*B + k] = global id of the k-th sample on
 rank r; rank_tokens[r]; send_samples[src*W + dst]; send_tokens[src*W + dst].
 
@@ -24,7 +28,12 @@ spread <= Lmax - Lmin, brute force agreement of the two enumerators, the
 counterexample [1,2,3,4] (paper 4/6 vs optimum 5/5), W=1 and B=1 special cases.
 LPT: never above the paper's maximum (by construction, checked), equal to the brute-force
 optimum where the greedy provably is (B = 1: one sample per rank; all lengths equal), a
-hand-worked instance, and max <= OPT + Lmax on random tiny inputs.  Parity pinned.
+hand-worked instance, and max <= OPT + Lmax on random tiny inputs.  relabel_locality: a
+hand-worked instance, the optimum equals scipy's linear_sum_assignment (Hungarian method, an
+independent library routine) on the same W x W matrix, every rank's load and sample order
+unchanged up to the labeling, never fewer kept tokens than the identity labeling.
+balance_stay: hand-worked instance, W = 1 / equal-lengths special cases (no swap), cardinality,
+max load never above the unbalanced maximum, every moved sample belongs to a swap pair.  Parity pinned.
 """
 from __future__ import annotations
 
@@ -202,6 +211,80 @@ def balance_opt(all_lengths, W, B, enumerator="recursive"):
             best_val, best_perm, best_groups = val, perm, groups
     out = plan_from_groups(a, W, B, [list(g) for g in best_groups])
     out["opt_max_tokens"] = best_val
+    return out
+
+
+def balance_stay(all_lengths, W, B):
+    """Beyond the paper (reading R25, NEXT-2 "locality-aware"): balance by moving as few
+    samples as possible.  The steps, in order:
+      1. every rank keeps its own samples (group r = ids r*B .. r*B + B - 1);
+      2. R20's step 2 on tokens (c = L), unchanged: up to 4*W*B times, M = most loaded rank
+         (lowest index on ties), m = least loaded (lowest index on ties); over x in M, y in m
+         with d = L[x] - L[y] > 0 take the pair minimising max(load[M] - d, load[m] + d), ties
+         by (x, y) ascending; stop unless it beats load[M]; swap x and y;
+      3. each rank lists its ids by (length asc, id asc).
+    Every swap moves two samples; no floor by the paper's plan (that would move ~all tokens)."""
+    a = _check(all_lengths, W, B)
+    groups = [list(range(r * B, (r + 1) * B)) for r in range(W)]
+    load = [sum(a[g] for g in grp) for grp in groups]
+    for _ in range(4 * W * B):
+        if W == 1:
+            break
+        M = max(range(W), key=lambda q: (load[q], -q))
+        m = min(range(W), key=lambda q: (load[q], q))
+        if M == m:
+            break
+        best = None
+        for x in groups[M]:
+            for y in groups[m]:
+                d = a[x] - a[y]
+                if d <= 0:
+                    continue
+                key = (max(load[M] - d, load[m] + d), x, y)
+                if best is None or key < best:
+                    best = key
+        if best is None or best[0] >= load[M]:
+            break
+        _, x, y = best
+        d = a[x] - a[y]
+        groups[M][groups[M].index(x)] = y
+        groups[m][groups[m].index(y)] = x
+        load[M] -= d
+        load[m] += d
+    return plan_from_groups(a, W, B, [sorted(grp, key=lambda g: (a[g], g)) for grp in groups])
+
+
+def kept_tokens(all_lengths, perm, W, B) -> int:
+    """Tokens that stay on their source rank under a plan: sum of L_g over samples g that rank
+    g // B keeps (the all-to-all-v moves every other token, P:359)."""
+    a = list(all_lengths)
+    return int(sum(a[int(perm[r * B + k])] for r in range(W) for k in range(B) if int(perm[r * B + k]) // B == r))
+
+
+def relabel_locality(all_lengths, perm, W, B):
+    """NEXT-2 beyond the paper (reading R24): the W groups of a plan (rank r's samples
+    perm[r*B : r*B+B]) may be handed to the ranks in any order without changing any rank's
+    load -- P:359's "worker i takes slice i" is one of W! labelings.  Choose the labeling that
+    keeps the most tokens on their source rank: group i goes to rank sigma[i], maximising
+    sum_i M[i][sigma[i]] with M[i][r] = tokens of group i whose source rank (g // B) is r.
+    Exhaustive over all W! labelings in lexicographic order of sigma (itertools), the first
+    maximum wins (ties -> lexicographically smallest sigma).  Returns the new perm (rank
+    sigma[i] lists group i in its original order)."""
+    a = list(all_lengths)
+    M = [[0] * W for _ in range(W)]
+    for i in range(W):
+        for k in range(B):
+            g = int(perm[i * B + k])
+            M[i][g // B] += a[g]
+    best, best_sigma = -1, None
+    for sigma in itertools.permutations(range(W)):
+        v = sum(M[i][sigma[i]] for i in range(W))
+        if v > best:
+            best, best_sigma = v, sigma
+    out = np.zeros(W * B, dtype=np.int64)
+    for i in range(W):
+        r = best_sigma[i]
+        out[r * B:(r + 1) * B] = [int(x) for x in perm[i * B:(i + 1) * B]]
     return out
 
 

@@ -14,7 +14,7 @@ STATUS_NAMES = {0: "UB_OK", 1: "UB_ERR_INVALID_ARG", 2: "UB_ERR_INVALID_MASK", 3
 UB_BF16, UB_FP32 = 0, 1
 UB_IPC_HANDLE_BYTES = 128
 UB_COMM_FORCE_NCCL = 1
-UB_BAL_PAPER, UB_BAL_SNAKE, UB_BAL_EXACT_SMALL, UB_BAL_LPT = 0, 1, 2, 3
+UB_BAL_PAPER, UB_BAL_SNAKE, UB_BAL_EXACT_SMALL, UB_BAL_LPT, UB_BAL_STAY = 0, 1, 2, 3, 4
 
 # every symbol include/ub.h declares, with (restype, argtypes)
 i32, i64, u64, f32, vp, sz = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_void_p, C.c_size_t
@@ -58,6 +58,7 @@ SIGNATURES = {
     "ub_encoder_attn_bwd": (i32, [C.POINTER(EncoderParams)] + [vp] * 21),
     "ub_balance_plan": (i32, [vp, i32, i32, i32, i32, vp, vp, vp, vp]),
     "ub_balance_plan_weighted": (i32, [vp, i32, i32, i32, i64, i64, vp, vp]),
+    "ub_balance_relabel": (i32, [vp, i32, i32, vp, vp, vp]),
     "ub_exchange_tables": (i32, [vp, vp, i32, i32, i32, i32, vp, vp, vp, vp]),
     "ub_exchange_copy": (i32, [vp, vp, vp, vp, vp, i32, i64, i64, vp]),
     "ub_validate_cu_seqlens": (i32, [vp, i32, i32, i64, vp, vp]),

@@ -12,10 +12,20 @@ import math
 import numpy as np
 import torch
 
-from ._lib import (EncoderParams, UB_BAL_EXACT_SMALL, UB_BAL_LPT, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BF16, UB_FP32,
+from ._lib import (EncoderParams, UB_BAL_EXACT_SMALL, UB_BAL_LPT, UB_BAL_PAPER, UB_BAL_SNAKE, UB_BAL_STAY, UB_BF16, UB_FP32,
                    UB_IPC_HANDLE_BYTES, FmhaParams, check, lib)
 
-BAL_MODES = {"paper": UB_BAL_PAPER, "snake": UB_BAL_SNAKE, "exact_small": UB_BAL_EXACT_SMALL, "lpt": UB_BAL_LPT}
+BAL_MODES = {"paper": UB_BAL_PAPER, "snake": UB_BAL_SNAKE, "exact_small": UB_BAL_EXACT_SMALL, "lpt": UB_BAL_LPT,
+             "stay": UB_BAL_STAY}
+UB_BAL_LOCALITY = 0x100
+
+
+def _mode(mode: str) -> int:
+    """'paper', 'snake', 'lpt', 'exact_small', each optionally '+locality' (UB_BAL_LOCALITY)."""
+    base, _, flag = mode.partition("+")
+    if flag not in ("", "locality"):
+        raise ValueError(f"bad balance mode {mode!r}")
+    return BAL_MODES[base] | (UB_BAL_LOCALITY if flag else 0)
 
 
 def _ptr(t):
@@ -278,9 +288,18 @@ def balance_plan(all_lengths, W: int, B: int, max_seqlen: int, mode: str = "pape
     rt = np.zeros(W, dtype=np.int64)
     ss = np.zeros(W * W, dtype=np.int32)
     st = np.zeros(W * W, dtype=np.int64)
-    check(lib().ub_balance_plan(_np_ptr(a), W, B, int(max_seqlen), BAL_MODES[mode], _np_ptr(perm), _np_ptr(rt),
+    check(lib().ub_balance_plan(_np_ptr(a), W, B, int(max_seqlen), _mode(mode), _np_ptr(perm), _np_ptr(rt),
                                 _np_ptr(ss), _np_ptr(st)))
     return {"perm": perm, "rank_tokens": rt, "send_samples": ss, "send_tokens": st}
+
+
+def balance_relabel(all_lengths, perm, W: int, B: int):
+    """Locality relabeling of a plan (R24): returns (new perm, kept tokens before, after)."""
+    a = np.ascontiguousarray(np.asarray(all_lengths, dtype=np.int32).reshape(-1))
+    p = np.ascontiguousarray(np.asarray(perm, dtype=np.int32)).copy()
+    kb, ka = C.c_int64(0), C.c_int64(0)
+    check(lib().ub_balance_relabel(_np_ptr(a), W, B, _np_ptr(p), C.byref(kb), C.byref(ka)))
+    return p, int(kb.value), int(ka.value)
 
 
 def balance_plan_weighted(all_lengths, W: int, B: int, max_seqlen: int, alpha: int, beta: int) -> dict:
@@ -429,7 +448,7 @@ class Comm:
                         f"exchange{self.rank}")
         perm = np.zeros(self.world * B, dtype=np.int32)
         T_out = C.c_int64(0)
-        check(lib().ub_balance_exchange(self.handle, BAL_MODES[mode], B, int(max_seqlen), _ptr(d_lengths),
+        check(lib().ub_balance_exchange(self.handle, _mode(mode), B, int(max_seqlen), _ptr(d_lengths),
                                         _ptr(d_tokens), _ptr(d_samples), rec, srec, int(capacity_tokens),
                                         _ptr(out_tokens), _ptr(out_samples), _ptr(out_cu), _np_ptr(perm),
                                         C.byref(T_out), _ptr(ws), _stream(stream)))
@@ -455,7 +474,7 @@ class Comm:
         ws = self._ws(B, capacity_tokens, rec, srec, out_tokens.device)
         perm = np.zeros(self.world * B, dtype=np.int32)
         T_out = C.c_int64(0)
-        check(lib().ub_exchange_finish(self.handle, int(slot), BAL_MODES[mode], B, int(max_seqlen), _ptr(d_tokens),
+        check(lib().ub_exchange_finish(self.handle, int(slot), _mode(mode), B, int(max_seqlen), _ptr(d_tokens),
                                        _ptr(d_samples), rec, srec, int(capacity_tokens), _ptr(out_tokens),
                                        _ptr(out_samples), _ptr(out_cu), _np_ptr(perm), C.byref(T_out), _ptr(ws),
                                        _stream(stream)))

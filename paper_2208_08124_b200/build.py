@@ -56,14 +56,18 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
-    """trace=True builds libub_trace.so with -DUB_TRACE (debug timelines; not the product)."""
-    build_dir = BUILD + ("_trace" if trace else "")
-    lib = LIB.replace("libub.so", "libub_trace.so") if trace else LIB
+def build(force: bool = False, verbose: bool = False, trace: bool = False, variant: str = "",
+          defines=()) -> str:
+    """trace=True builds libub_trace.so with -DUB_TRACE (debug timelines; not the product).
+    variant="x", defines=["A=1"] builds libub_x.so with -DA=1 (dev A/B experiments only)."""
+    tag = "trace" if trace else variant
+    build_dir = BUILD + ("_" + tag if tag else "")
+    lib = LIB.replace("libub.so", f"libub_{tag}.so") if tag else LIB
     os.makedirs(build_dir, exist_ok=True)
     nccl, flags = _flags()
     if trace:
         flags = flags + ["-DUB_TRACE"]
+    flags = flags + ["-D" + d for d in defines]
     hdrs = _headers()
     jobs = []
     objs = []
@@ -96,4 +100,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))
+    var = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")]
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv,
+                variant=var[0] if var else "", defines=defs))

@@ -73,29 +73,13 @@ struct ExactSearch {  // exhaustive min-max partition search for W*B <= 12 (R15 
   }
 };
 
-// Cardinality-constrained LPT with (max, min) swap refinement on an integer per-sample cost
-// (NEXT-2 of SURVEY §8(f); DESIGN.md "balancer modes").  Steps, as oracle/balance.py:
-//   1. ids by (cost desc, id asc); each goes to the open rank (fewer than B samples) with the
-//      least load, lowest rank on ties;
-//   2. repeat (at most 4*W*B times): M = most loaded rank, m = least loaded (lowest index on
-//      ties); among pairs x in M, y in m with d = c[x] - c[y] > 0 take the one minimising
-//      max(load[M] - d, load[m] + d), ties by (x, y) ascending; stop unless that is < load[M];
-//   3. if the paper's interleave (same cost) has a strictly smaller maximum, use it instead;
-//   4. each rank lists its samples by (length asc, id asc), the paper's order (R12).
-void plan_lpt(const int32_t* a, const std::vector<int64_t>& c, int32_t W, int32_t B, int32_t* perm) {
+// R20 step 2 (also R25 step 2): repeat (at most 4*W*B times): M = most loaded rank, m = least
+// loaded (lowest index on ties); among pairs x in M, y in m with d = c[x] - c[y] > 0 take the
+// one minimising max(load[M] - d, load[m] + d), ties by (x, y) ascending; stop unless that is
+// < load[M]; swap x and y.
+void swap_refine(const std::vector<int64_t>& c, int32_t W, int32_t B, std::vector<std::vector<int32_t>>& grp,
+                 std::vector<int64_t>& load) {
   const int32_t n = W * B;
-  std::vector<int32_t> order(n);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&c](int32_t x, int32_t y) { return c[x] > c[y]; });
-  std::vector<std::vector<int32_t>> grp(W);
-  std::vector<int64_t> load(W, 0);
-  for (int32_t g : order) {
-    int32_t best = -1;
-    for (int32_t r = 0; r < W; ++r)
-      if ((int32_t)grp[r].size() < B && (best < 0 || load[r] < load[best])) best = r;
-    grp[best].push_back(g);
-    load[best] += c[g];
-  }
   for (int32_t iter = 0; iter < 4 * n && W > 1; ++iter) {
     int32_t M = 0, m = 0;
     for (int32_t r = 1; r < W; ++r) {
@@ -122,6 +106,32 @@ void plan_lpt(const int32_t* a, const std::vector<int64_t>& c, int32_t W, int32_
     load[M] -= d;
     load[m] += d;
   }
+}
+
+// Cardinality-constrained LPT with (max, min) swap refinement on an integer per-sample cost
+// (NEXT-2 of SURVEY §8(f); DESIGN.md "balancer modes").  Steps, as oracle/balance.py:
+//   1. ids by (cost desc, id asc); each goes to the open rank (fewer than B samples) with the
+//      least load, lowest rank on ties;
+//   2. repeat (at most 4*W*B times): M = most loaded rank, m = least loaded (lowest index on
+//      ties); among pairs x in M, y in m with d = c[x] - c[y] > 0 take the one minimising
+//      max(load[M] - d, load[m] + d), ties by (x, y) ascending; stop unless that is < load[M];
+//   3. if the paper's interleave (same cost) has a strictly smaller maximum, use it instead;
+//   4. each rank lists its samples by (length asc, id asc), the paper's order (R12).
+void plan_lpt(const int32_t* a, const std::vector<int64_t>& c, int32_t W, int32_t B, int32_t* perm) {
+  const int32_t n = W * B;
+  std::vector<int32_t> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&c](int32_t x, int32_t y) { return c[x] > c[y]; });
+  std::vector<std::vector<int32_t>> grp(W);
+  std::vector<int64_t> load(W, 0);
+  for (int32_t g : order) {
+    int32_t best = -1;
+    for (int32_t r = 0; r < W; ++r)
+      if ((int32_t)grp[r].size() < B && (best < 0 || load[r] < load[best])) best = r;
+    grp[best].push_back(g);
+    load[best] += c[g];
+  }
+  swap_refine(c, W, B, grp, load);
   // the paper's interleave as a floor
   const auto ids = sorted_ids(a, n);
   int64_t paper_max = 0, lpt_max = 0;
@@ -142,10 +152,83 @@ void plan_lpt(const int32_t* a, const std::vector<int64_t>& c, int32_t W, int32_
   }
 }
 
+// Reading R24: hand the W groups to the ranks maximising the tokens kept at home.  g[mask] =
+// best kept tokens of groups popcount(mask)..W-1 placed on the ranks outside mask; the
+// reconstruction takes, group by group, the smallest rank that attains the optimum, which
+// yields the lexicographically smallest optimal sigma (the oracle's first maximum in
+// lexicographic permutation order).
+// Reading R25 (NEXT-2, locality-aware): every rank starts with its own samples, R20's swap
+// refinement on tokens balances them, each rank lists its ids by (length asc, id asc).
+void plan_stay(const int32_t* a, int32_t W, int32_t B, int32_t* perm) {
+  std::vector<int64_t> c(a, a + (size_t)W * B);
+  std::vector<std::vector<int32_t>> grp(W);
+  std::vector<int64_t> load(W, 0);
+  for (int32_t r = 0; r < W; ++r)
+    for (int32_t k = 0; k < B; ++k) {
+      grp[r].push_back(r * B + k);
+      load[r] += a[r * B + k];
+    }
+  swap_refine(c, W, B, grp, load);
+  for (int32_t r = 0; r < W; ++r) {
+    std::sort(grp[r].begin(), grp[r].end(), [a](int32_t x, int32_t y) { return a[x] != a[y] ? a[x] < a[y] : x < y; });
+    for (int32_t k = 0; k < B; ++k) perm[r * B + k] = grp[r][k];
+  }
+}
+
+void relabel_groups(const int32_t* a, int32_t W, int32_t B, int32_t* perm, int64_t* before, int64_t* after) {
+  std::vector<int64_t> M((size_t)W * W, 0);
+  int64_t kept0 = 0;
+  for (int32_t i = 0; i < W; ++i)
+    for (int32_t k = 0; k < B; ++k) {
+      const int32_t g = perm[i * B + k];
+      M[(size_t)i * W + g / B] += a[g];
+      if (g / B == i) kept0 += a[g];
+    }
+  const uint32_t full = (W >= 32) ? 0xFFFFFFFFu : ((1u << W) - 1u);
+  std::vector<int64_t> best((size_t)full + 1, 0);
+  for (int64_t mask = (int64_t)full - 1; mask >= 0; --mask) {
+    const int32_t i = __builtin_popcount((uint32_t)mask);
+    int64_t v = -1;
+    for (int32_t r = 0; r < W; ++r)
+      if (!((uint32_t)mask >> r & 1u)) v = std::max(v, M[(size_t)i * W + r] + best[(size_t)mask | (1u << r)]);
+    best[(size_t)mask] = v;
+  }
+  std::vector<int32_t> sigma(W);
+  uint32_t mask = 0;
+  for (int32_t i = 0; i < W; ++i)
+    for (int32_t r = 0; r < W; ++r)
+      if (!(mask >> r & 1u) && M[(size_t)i * W + r] + best[mask | (1u << r)] == best[mask]) {
+        sigma[i] = r;
+        mask |= 1u << r;
+        break;
+      }
+  std::vector<int32_t> old(perm, perm + (size_t)W * B);
+  for (int32_t i = 0; i < W; ++i)
+    std::copy(old.begin() + (size_t)i * B, old.begin() + (size_t)(i + 1) * B, perm + (size_t)sigma[i] * B);
+  if (before) *before = kept0;
+  if (after) *after = best[0];
+}
+
 }  // namespace
 }  // namespace ub
 
 using namespace ub;
+
+extern "C" ub_status ub_balance_relabel(const int32_t* a, int32_t W, int32_t B, int32_t* perm, int64_t* kept_before,
+                                        int64_t* kept_after) {
+  clear_error();
+  UB_REQUIRE(a && perm, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(W >= 1 && B >= 1, UB_ERR_INVALID_ARG, "W=%d B=%d", W, B);
+  UB_REQUIRE(W <= 20, UB_ERR_UNSUPPORTED, "locality relabeling needs W <= 20 (got %d)", W);
+  std::vector<char> seen((size_t)W * B, 0);
+  for (int32_t i = 0; i < W * B; ++i) {
+    UB_REQUIRE(perm[i] >= 0 && perm[i] < W * B && !seen[perm[i]], UB_ERR_SHAPE, "perm is not a permutation");
+    seen[perm[i]] = 1;
+    UB_REQUIRE(a[perm[i]] >= 0, UB_ERR_INVALID_ARG, "negative length");
+  }
+  relabel_groups(a, W, B, perm, kept_before, kept_after);
+  return UB_OK;
+}
 
 extern "C" ub_status ub_balance_plan(const int32_t* a, int32_t W, int32_t B, int32_t max_seqlen, int32_t mode,
                                      int32_t* perm, int64_t* rank_tokens, int32_t* send_samples,
@@ -159,6 +242,9 @@ extern "C" ub_status ub_balance_plan(const int32_t* a, int32_t W, int32_t B, int
     UB_REQUIRE(a[g] >= 1, UB_ERR_INVALID_ARG, "length[%d] = %d < 1", g, a[g]);
     UB_REQUIRE(a[g] <= max_seqlen, UB_ERR_CAPACITY, "length[%d] = %d > max_seqlen %d", g, a[g], max_seqlen);
   }
+  const bool locality = (mode & UB_BAL_LOCALITY) != 0;
+  mode &= ~UB_BAL_LOCALITY;
+  UB_REQUIRE(!locality || W <= 20, UB_ERR_UNSUPPORTED, "UB_BAL_LOCALITY needs W <= 20 (got %d)", W);
   if (mode == UB_BAL_PAPER) {
     const auto ids = sorted_ids(a, n);
     for (int32_t i = 0; i < W; ++i)                 // worker i takes i, i+W, i+2W, ...
@@ -173,6 +259,8 @@ extern "C" ub_status ub_balance_plan(const int32_t* a, int32_t W, int32_t B, int
   } else if (mode == UB_BAL_LPT) {
     std::vector<int64_t> c(a, a + n);
     plan_lpt(a, c, W, B, perm);
+  } else if (mode == UB_BAL_STAY) {
+    plan_stay(a, W, B, perm);
   } else if (mode == UB_BAL_EXACT_SMALL) {
     UB_REQUIRE(n <= 12, UB_ERR_UNSUPPORTED, "UB_BAL_EXACT_SMALL needs W*B <= 12 (got %d)", n);
     ExactSearch es{a, W, B, n};
@@ -183,6 +271,7 @@ extern "C" ub_status ub_balance_plan(const int32_t* a, int32_t W, int32_t B, int
   } else {
     return set_error(UB_ERR_INVALID_ARG, "bad balance mode %d", mode);
   }
+  if (locality) relabel_groups(a, W, B, perm, nullptr, nullptr);
   if (rank_tokens)
     for (int32_t r = 0; r < W; ++r) {
       int64_t t = 0;

@@ -21,21 +21,27 @@
 //
 // CTA = 16 warps (1 per SM), four warpgroups:
 //   warps 0-7   two compute warpgroups: thread r of warpgroup x owns key row r and query
-//               columns [64x, 64x+64) of S^T / dP^T
-//   warps 8-11  epilogue warpgroup: dQ_i out of TMEM, and dK / dV at the end of a pass
+//               columns [64x, 64x+64) of S^T / dP^T; per pair two phases:
+//                 A: S^T -> P (exp2), P~ (dropout) -> bf16 over its own S^T columns
+//                 B: dP^T -> dS = P (dP~ M/(1-p) - Delta) -> bf16 over its own dP^T columns
+//                    and into smem (the A operand of dQ)
+//   warps 8-11  epilogue warpgroup: dQ_i out of TMEM (two buffers), dK / dV at a pass end
 //   warp 12     producer of Q, dO per query tile (3 stages) by TMA; the tile's LSE / Delta
 //               vectors by the 32 lanes into smem
 //   warp 13     TMEM allocator, then MMA issuer (one thread)
 //   warp 14     producer of K, V per pass (double-buffered); warp 15 idle
 // Registers: 128 per thread at launch; setmaxnreg moves them to the compute warpgroups
-// (168) and the epilogue (112) from the producer / MMA warps (64): 2 x 168 + 112 + 64 = 4 x 128
-// (64 rather than 56 for the MMA issuer: 20 -> 6 spill instructions, -1 % time).
-// TMEM columns: S^T 0..127, dP^T 128..255, P~^T 256..319 (bf16 pairs), dQ 320..383,
+// (168) and the epilogue (112) from the producer / MMA warps (64): 2 x 168 + 112 + 64 = 4 x 128.
+// TMEM columns: S^T 0..127 (P~^T bf16 pairs over it: warpgroup x at 64x..64x+31), dP^T
+// 128..255 (dS^T bf16 pairs over it: 128+64x..+31), dQ two buffers 256..319 / 320..383,
 // dV 384..447, dK 448..511.
-// The MMA issues S_{p+1}, dP_{p+1} as soon as the compute warps have loaded S_p, dP_p, so
-// the exp/dS phase of pair p overlaps the tensor work of pair p+1; the compute warps write
-// P~_{p+1} / dS_{p+1} once grads_p (dV, dK, dQ) have completed, and dQ_{p+1} is issued once
-// the epilogue has read dQ_p -- the epilogue is one pair behind, off the critical path.
+// MMA order per pair p (one thread, tcgen05 ops execute in issue order):
+//     dV_p += P~_p^T dO_p (TS) | S_{p+1} | dK_p += dS_p^T Q_p (TS) | dQ_p = dS_p K (SS) | dP_{p+1}
+// S_{p+1} overwrites the P~_p columns only after dV_p has read them and dP_{p+1} the dS_p
+// columns only after dK_p (issue order); a completion commit after dP_{p+1} also covers dQ_p,
+// so the compute warps' next dS store to smem never races dQ_p's read.  Phase A of pair
+// p+1 (the exp2 work) runs while the tensor core does dK_p, dQ_p, dP_{p+1}; phase B of pair p
+// while it does dV_p, S_{p+1}.
 #include <cmath>
 
 #include "fmha_common.cuh"
@@ -59,7 +65,15 @@ constexpr uint32_t kTileBytes = kTile * kD * 2;   // 16 KB
 constexpr uint32_t kPBytes = kTile * kTile * 2;   // 32 KB
 constexpr int kThreads = 512;
 constexpr uint32_t kQStages = 3;                  // Q / dO / LSE / Delta pipeline depth
-constexpr uint32_t kColS = 0, kColDP = 128, kColP = 256, kColDQ = 320, kColDV = 384, kColDK = 448;
+#ifndef UB_BWD_POLY
+#define UB_BWD_POLY 0
+#endif
+constexpr int kPolyPairs = UB_BWD_POLY;           // exp2 pairs of every 8 on the FMA pipe (phase A); measured 0 / 1 / 2 / 3 -> 106.5 / 107.1 / 107.2 / 108.2 us: MUFU does not bind
+constexpr uint32_t kColS = 0, kColDP = 128, kColDQ = 256, kColDV = 384, kColDK = 448;   // dQ: 2 x 64
+// TMEM column of the k-th K=16 slice of a TS MMA's A operand held as bf16 pairs over the
+// S^T / dP^T block at `base`: queries 0..63 sit at base+0..31 (warpgroup 0), 64..127 at
+// base+64..95 (warpgroup 1), so that each warpgroup overwrites only its own fp32 columns
+__device__ __forceinline__ uint32_t a_col(uint32_t base, uint32_t k) { return base + (k < 4 ? k * 8 : 64 + (k - 4) * 8); }
 
 struct Smem {
   uint8_t k[2][kTileBytes];
@@ -69,11 +83,11 @@ struct Smem {
   uint8_t ds[kPBytes];              // dS^T [key][query], 2 x 64-query SW128 regions
   uint8_t stage[4][4096];           // per epilogue warp: [32 rows][128 B], 128-B swizzle: half of
                                     // dQ (32 fp32 columns), or dK, or dV (64 bf16)
-  float lse[kQStages][kTile];       // LSE of the query tile's rows (natural log)
+  float lse[kQStages][kTile];       // -LSE * log2(e) of the query tile's rows; -inf past the sequence
   float delta[kQStages][kTile];
   uint64_t kv_full[2], kv_empty[2];
   uint64_t qdo_full[kQStages], qdo_empty[kQStages];
-  uint64_t s_full, s_free, pds_full, dq_full, dq_empty, dkv_full, dkv_free;
+  uint64_t s_full, dp_full, p_full, ds_full, dq_full[2], dq_empty[2], dkv_full, dkv_free;
   uint32_t tmem_base;
   PlanSmem plan;
   ItemTable items;                  // this CTA's items, decoded once
@@ -146,10 +160,13 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       mbar_init(&sm.qdo_empty[s], 1);
     }
     mbar_init(&sm.s_full, 1);
-    mbar_init(&sm.s_free, 8);
-    mbar_init(&sm.pds_full, 8);
-    mbar_init(&sm.dq_full, 1);
-    mbar_init(&sm.dq_empty, 4);
+    mbar_init(&sm.dp_full, 1);
+    mbar_init(&sm.p_full, 8);
+    mbar_init(&sm.ds_full, 8);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.dq_full[b], 1);
+      mbar_init(&sm.dq_empty[b], 4);
+    }
     mbar_init(&sm.dkv_full, 1);
     mbar_init(&sm.dkv_free, 4);
     fence_mbar_init();
@@ -203,13 +220,16 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           const uint32_t st = qit % kQStages, ph = (qit / kQStages) & 1;
           const int32_t q0 = it.c0 + i * kTile;
           // LSE / Delta loads are issued before the stage wait so their latency hides behind it
+          // stored as -LSE * log2(e) (the compute warps' exp2 argument is scale_log2 * S + this),
+          // and -inf / 0 for query rows past the sequence end: their P = exp2(-inf) = 0 and dS = 0
+          // without any per-element mask in the compute warps
           float lv[4], dv[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int32_t k = (int32_t)lane + 32 * u;
             const bool ok = i * kTile + k < it.L;
             const int64_t idx = (int64_t)it.h * prm.T + q0 + k;
-            lv[u] = ok ? __ldg(prm.lse + idx) : 0.f;
+            lv[u] = ok ? -1.4426950408889634f * __ldg(prm.lse + idx) : -INFINITY;
             dv[u] = ok ? __ldg(prm.delta + idx) : 0.f;
           }
           TR(22);
@@ -234,77 +254,104 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     }
   } else if (warp == 13) {
     // ------------------------------------------------------------ MMA issuer
-    // One pipeline over all (item, pass, query tile) pairs: S_p, dP_p are issued before the
-    // grads of pair p-1, also across pass and item boundaries.
+    // One pipeline over all (item, pass, query tile) pairs of the CTA, also across pass and
+    // item boundaries: dV_p | S_{p+1} | dK_p | dQ_p | dP_{p+1} (see the header).
     if (lane == 0) {
-      uint32_t pass = 0, qit = 0, s_cnt = 0, g_cnt = 0;
       const uint32_t ds_addr = smem_u32(sm.ds);
-      bool pend = false, p_first = false, p_last = false;    // the pair whose grads are pending
-      uint32_t p_st = 0, p_kaddr = 0, p_kvs = 0, p_pass = 0;
-      auto grads = [&]() {
-        mbar_wait(&sm.pds_full, g_cnt & 1);
-        if (p_first) mbar_wait(&sm.dkv_free, (p_pass & 1) ^ 1);
-        TR(12);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(sm.q[p_st]), do_addr = smem_u32(sm.dO[p_st]);
-#pragma unroll
-        for (uint32_t k = 0; k < kTile / 16; ++k)        // dV += P~^T dO, K = query rows, 16 per MMA
-          umma_bf16_ts(tmem + kColDV, tmem + kColP + k * 8, sdesc_sw128(do_addr + k * 2048, 8192, 1024), kIdescTS,
-                       (p_first && k == 0) ? 0u : 1u);
-#pragma unroll
-        for (uint32_t k = 0; k < kTile / 16; ++k)        // dK += dS^T Q, A = dS^T K-major from smem
-          umma_bf16_ss(tmem + kColDK, sdesc_sw128(ds_addr + (k >> 2) * (kTile * 128) + (k & 3) * 32, 16, 1024),
-                       sdesc_sw128(q_addr + k * 2048, 8192, 1024), kIdescTS, (p_first && k == 0) ? 0u : 1u);
-        umma_commit(&sm.qdo_empty[p_st]);              // Q_i / dO_i no longer needed
-        mbar_wait(&sm.dq_empty, (g_cnt & 1) ^ 1);      // the epilogue has read dQ of the previous pair
-        tc_fence_after();
-#pragma unroll
-        for (uint32_t k = 0; k < kTile / 16; ++k)        // dQ = dS K, K = key rows, 16 per MMA
-          umma_bf16_ss(tmem + kColDQ, sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024),
-                       sdesc_sw128(p_kaddr + k * 2048, 8192, 1024), kIdescQ, k > 0);
-        umma_commit(&sm.dq_full);                      // grads done: P~^T / dS free, dQ_i in TMEM
-        TR(19);
-        ++g_cnt;
-        if (p_last) {                                  // the pass's K, V and dK, dV are final
-          umma_commit(&sm.kv_empty[p_kvs]);
-          umma_commit(&sm.dkv_full);
-        }
-      };
+      // the pair sequence, walked one pair ahead of issue
+      struct Pair { int32_t kt, i, nt; uint32_t q, st, kvs, pass; bool first, last; };
       WorkItem it;
-      UB_ITEMS(r, it) {
-        for (int32_t kt = 0; kt < it.nt; ++kt, ++pass) {
-          const uint32_t kvs = pass & 1;
-          const uint32_t k_addr = smem_u32(sm.k[kvs]), v_addr = smem_u32(sm.v[kvs]);
-          TR(16);
-          mbar_wait(&sm.kv_full[kvs], (pass >> 1) & 1);
-          TR(17);
-          for (int32_t i = 0; i < it.nt; ++i, ++qit) {
-            const uint32_t st = qit % kQStages;
-            mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);
-            TR(18);
-            mbar_wait(&sm.s_free, (s_cnt & 1) ^ 1);
-            TR(10);
-            tc_fence_after();
-            const uint32_t q_addr = smem_u32(sm.q[st]), do_addr = smem_u32(sm.dO[st]);
-#pragma unroll
-            for (uint32_t k = 0; k < kD / 16; ++k) {
-              umma_bf16_ss(tmem + kColS, sdesc_sw128(k_addr + k * 32, 16, 1024), sdesc_sw128(q_addr + k * 32, 16, 1024),
-                           kIdescS, k > 0);
-              umma_bf16_ss(tmem + kColDP, sdesc_sw128(v_addr + k * 32, 16, 1024),
-                           sdesc_sw128(do_addr + k * 32, 16, 1024), kIdescS, k > 0);
-            }
-            umma_commit(&sm.s_full);
-            TR(11);
-            ++s_cnt;
-            if (pend) grads();
-            pend = true;
-            p_st = st; p_kaddr = k_addr; p_kvs = kvs; p_pass = pass;
-            p_first = i == 0;
-            p_last = i == it.nt - 1;
+      int32_t r = 0, kt = 0, i = 0;
+      uint32_t qit = 0, pass = 0;
+      bool have = next_item<kBigB>(0, sm.items, sm.plan, prm.plan, prm.cu, prm.B, H, 0, cta, G, it);
+      auto advance = [&](Pair& pr) -> bool {           // the next pair in CTA order, or false
+        if (!have) return false;
+        pr.kt = kt; pr.i = i; pr.nt = it.nt; pr.q = qit; pr.st = qit % kQStages; pr.kvs = pass & 1; pr.pass = pass;
+        pr.first = i == 0; pr.last = i == it.nt - 1;
+        ++qit;
+        if (++i == it.nt) {
+          i = 0; ++pass;
+          if (++kt == it.nt) {
+            kt = 0;
+            have = next_item<kBigB>(++r, sm.items, sm.plan, prm.plan, prm.cu, prm.B, H, 0, cta, G, it);
           }
         }
+        return true;
+      };
+      auto issue_s_dp = [&](const Pair& pr, bool s_part) {  // S^T = K Q^T or dP~^T = V dO^T
+        const uint32_t a = smem_u32(s_part ? sm.k[pr.kvs] : sm.v[pr.kvs]);
+        const uint32_t b = smem_u32(s_part ? sm.q[pr.st] : sm.dO[pr.st]);
+#pragma unroll
+        for (uint32_t k = 0; k < kD / 16; ++k)
+          umma_bf16_ss(tmem + (s_part ? kColS : kColDP), sdesc_sw128(a + k * 32, 16, 1024),
+                       sdesc_sw128(b + k * 32, 16, 1024), kIdescS, k > 0);
+      };
+      auto wait_inputs = [&](const Pair& pr) {          // K/V of its pass, Q/dO of its tile
+        if (pr.first) mbar_wait(&sm.kv_full[pr.kvs], (pr.pass >> 1) & 1);
+        mbar_wait(&sm.qdo_full[pr.st], (pr.q / kQStages) & 1);
+      };
+      Pair cur, nxt;
+      uint32_t p = 0;
+      bool has_cur = advance(cur);
+      if (has_cur) {
+        wait_inputs(cur);
+        tc_fence_after();
+        issue_s_dp(cur, true);
+        umma_commit(&sm.s_full);
+        issue_s_dp(cur, false);
+        umma_commit(&sm.dp_full);
       }
-      if (pend) grads();
+      while (has_cur) {
+        const uint32_t q_addr = smem_u32(sm.q[cur.st]), do_addr = smem_u32(sm.dO[cur.st]);
+        const uint32_t k_addr = smem_u32(sm.k[cur.kvs]);
+        // dV_p += P~_p^T dO_p (A = P~^T bf16 pairs over the S^T columns)
+        mbar_wait(&sm.p_full, p & 1);
+        if (cur.first) mbar_wait(&sm.dkv_free, (cur.pass & 1) ^ 1);   // previous pass's dK / dV drained
+        TR(12);
+        tc_fence_after();
+#pragma unroll
+        for (uint32_t k = 0; k < kTile / 16; ++k)
+          umma_bf16_ts(tmem + kColDV, tmem + a_col(kColS, k), sdesc_sw128(do_addr + k * 2048, 8192, 1024), kIdescTS,
+                       (cur.first && k == 0) ? 0u : 1u);
+        // S_{p+1} (its Q / K inputs)
+        const bool has_nxt = advance(nxt);
+        if (has_nxt) {
+          wait_inputs(nxt);
+          tc_fence_after();
+          issue_s_dp(nxt, true);
+          umma_commit(&sm.s_full);
+        }
+        TR(10);
+        // dK_p += dS_p^T Q_p (A = dS^T bf16 pairs over the dP^T columns), dQ_p = dS_p K
+        mbar_wait(&sm.ds_full, p & 1);
+        tc_fence_after();
+#pragma unroll
+        for (uint32_t k = 0; k < kTile / 16; ++k)
+          umma_bf16_ts(tmem + kColDK, tmem + a_col(kColDP, k), sdesc_sw128(q_addr + k * 2048, 8192, 1024), kIdescTS,
+                       (cur.first && k == 0) ? 0u : 1u);
+        umma_commit(&sm.qdo_empty[cur.st]);              // Q_p / dO_p / LSE / Delta no longer needed
+        const uint32_t b = p & 1;
+        mbar_wait(&sm.dq_empty[b], ((p >> 1) & 1) ^ 1);  // the epilogue has drained this dQ buffer
+        tc_fence_after();
+#pragma unroll
+        for (uint32_t k = 0; k < kTile / 16; ++k)
+          umma_bf16_ss(tmem + kColDQ + 64 * b, sdesc_sw128(ds_addr + k * 2048, kTile * 128, 1024),
+                       sdesc_sw128(k_addr + k * 2048, 8192, 1024), kIdescQ, k > 0);
+        umma_commit(&sm.dq_full[b]);
+        if (cur.last) {                                  // the pass's K, V and dK, dV are final
+          umma_commit(&sm.kv_empty[cur.kvs]);
+          umma_commit(&sm.dkv_full);
+        }
+        TR(19);
+        // dP~_{p+1} (overwrites dS_p's columns after dK_p in issue order)
+        if (has_nxt) {
+          issue_s_dp(nxt, false);
+          umma_commit(&sm.dp_full);
+        }
+        ++p;
+        cur = nxt;
+        has_cur = has_nxt;
+      }
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ compute warpgroups
@@ -314,86 +361,120 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     const uint32_t t_row = tmem + (((warp & 3) * 32) << 16);
     const float c = prm.scale_log2;
     const uint64_t c2 = f2pack(c, c);
-    const uint64_t nl2e2 = f2pack(-1.4426950408889634f, -1.4426950408889634f);
     const uint32_t ds_addr = smem_u32(sm.ds) + x * (kTile * 128);
-    uint32_t s_cnt = 0, g_cnt = 0, qit = 0;
+    uint32_t p = 0, qit = 0;
     WorkItem it;
 
     UB_ITEMS(ri, it) {
       for (int32_t kt = 0; kt < it.nt; ++kt) {
         const int32_t key = kt * kTile + (int32_t)r;
         const bool key_ok = key < it.L;
+        const bool warp_partial = __any_sync(0xffffffffu, !key_ok);     // a sequence's last key tile
         const uint32_t warp_j0 = (uint32_t)(kt * kTile) + (warp & 3) * 32;   // the warp's first key
-        for (int32_t i = 0; i < it.nt; ++i, ++qit) {
+        for (int32_t i = 0; i < it.nt; ++i, ++qit, ++p) {
           const uint32_t st = qit % kQStages;
-          const int32_t qvalid = it.L - i * kTile;          // query rows of this tile inside the sequence
+          // ---- phase A: P = exp2(scale_log2 S - LSE log2 e), P~ = P M / (1-p) -> bf16 over S^T
           TR(1);
           mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);   // LSE / Delta of this query tile
-          mbar_wait(&sm.s_full, s_cnt & 1);
+          mbar_wait(&sm.s_full, p & 1);
           TR(2);
           tc_fence_after();
-          uint32_t sr[2][32], dr[2][32];
-          tmem_ld32(t_row + kColS + x * 64, sr[0]);
-          tmem_ld32(t_row + kColS + x * 64 + 32, sr[1]);
-          tmem_ld32(t_row + kColDP + x * 64, dr[0]);
-          tmem_ld32(t_row + kColDP + x * 64 + 32, dr[1]);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.s_free);
-          ++s_cnt;
-          TR(3);
-
-          uint32_t pp[32], pd[32];
+          float pf[64];                                     // P (fp32), kept for phase B
+          {
+            uint32_t sr[2][32];
+            tmem_ld32(t_row + kColS + x * 64, sr[0]);
+            tmem_ld32(t_row + kColS + x * 64 + 32, sr[1]);
+            tmem_ld_wait();
 #pragma unroll
-          for (int ch = 0; ch < 2; ++ch) {
-            const int q0 = (int)x * 64 + ch * 32;
-            uint32_t keep = 0xFFFFFFFFu;
-            if (kDropout) {
-              keep = 0;
-              const uint32_t tq = (uint32_t)(it.c0 + i * kTile + q0);
+            for (int ch = 0; ch < 2; ++ch)
 #pragma unroll
-              for (int b16 = 0; b16 < 2; ++b16) keep |= keep16_cols(warp_j0, tq + 16 * b16, it.h, prm, lane) << (16 * b16);
-            }
-#pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse[st][q0 + e]);
-              const float2 dl = *reinterpret_cast<const float2*>(&sm.delta[st][q0 + e]);
-              float pa, pb;
-              f2unpack(ffma2(f2pack(__uint_as_float(sr[ch][e]), __uint_as_float(sr[ch][e + 1])), c2,
-                             fmul2(f2pack(l2.x, l2.y), nl2e2)), pa, pb);
-              pa = (key_ok && q0 + e < qvalid) ? ex2f(pa) : 0.f;
-              pb = (key_ok && q0 + e + 1 < qvalid) ? ex2f(pb) : 0.f;
-              float dpa = __uint_as_float(dr[ch][e]), dpb = __uint_as_float(dr[ch][e + 1]);
-              float qa = pa, qb = pb;
-              if (kDropout) {
-                const bool ka = (keep >> e) & 1u, kb = (keep >> (e + 1)) & 1u;
-                qa = ka ? pa * prm.rp : 0.f;
-                qb = kb ? pb * prm.rp : 0.f;
-                dpa = ka ? dpa * prm.rp : 0.f;
-                dpb = kb ? dpb * prm.rp : 0.f;
+              for (int e = 0; e < 32; e += 2) {
+                // -LSE log2(e) of the two query columns (broadcast smem loads); the producer's
+                // -inf for columns past the sequence end makes P = dS = 0 there
+                const float2 l2 = *reinterpret_cast<const float2*>(&sm.lse[st][x * 64 + ch * 32 + e]);
+                float a, b;
+                f2unpack(ffma2(f2pack(__uint_as_float(sr[ch][e]), __uint_as_float(sr[ch][e + 1])), c2,
+                               f2pack(l2.x, l2.y)), a, b);
+                if (kPolyPairs > 0 && ((e >> 1) & 7) < kPolyPairs) {
+                  f2unpack(ex2_poly2(a, b), a, b);          // FMA pipe: MUFU is phase A's bound
+                } else {
+                  a = ex2f(a);
+                  b = ex2f(b);
+                }
+                pf[ch * 32 + e] = a;
+                pf[ch * 32 + e + 1] = b;
               }
-              float da, db;
-              f2unpack(fmul2(f2pack(pa, pb), fadd2(f2pack(dpa, dpb), f2pack(-dl.x, -dl.y))), da, db);
-              pp[ch * 16 + e / 2] = pack_bf16(qa, qb);
-              pd[ch * 16 + e / 2] = pack_bf16(da, db);
+          }
+          TR(3);
+          uint32_t keep[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
+          if (kDropout) {
+#pragma unroll
+            for (int ch = 0; ch < 2; ++ch) {
+              const uint32_t tq = (uint32_t)(it.c0 + i * kTile + (int)x * 64 + ch * 32);
+              keep[ch] = keep16_cols(warp_j0, tq, it.h, prm, lane) | (keep16_cols(warp_j0, tq + 16, it.h, prm, lane) << 16);
             }
           }
-          // grads of the previous pair done => P~^T TMEM and the dS smem tile are free
+          {
+            uint32_t pp[32];
+#pragma unroll
+            for (int e = 0; e < 64; e += 2) {
+              float qa = pf[e], qb = pf[e + 1];
+              if (kDropout) {
+                qa = ((keep[e >> 5] >> (e & 31)) & 1u) ? qa * prm.rp : 0.f;
+                qb = ((keep[e >> 5] >> ((e + 1) & 31)) & 1u) ? qb * prm.rp : 0.f;
+              }
+              pp[e / 2] = pack_bf16(qa, qb);
+            }
+            if (warp_partial) {                            // key rows past the sequence end
+#pragma unroll
+              for (int e = 0; e < 32; ++e) pp[e] = key_ok ? pp[e] : 0u;
+            }
+            tmem_st32(t_row + kColS + x * 64, pp);        // over this warpgroup's own S^T columns
+            tmem_st_wait();
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sm.p_full);
           TR(4);
-          mbar_wait(&sm.dq_full, (g_cnt & 1) ^ 1);
+          // ---- phase B: dS = P (dP~ M / (1-p) - Delta) -> bf16 over dP^T and into smem
+          mbar_wait(&sm.dp_full, p & 1);
           TR(5);
           tc_fence_after();
-          tmem_st32(t_row + kColP + x * 32, pp);
+          {
+            uint32_t dr[2][32];
+            tmem_ld32(t_row + kColDP + x * 64, dr[0]);
+            tmem_ld32(t_row + kColDP + x * 64 + 32, dr[1]);
+            tmem_ld_wait();
+            uint32_t pd[32];
 #pragma unroll
-          for (int g = 0; g < 8; ++g)
-            st_shared_v4(ds_addr + sw128_off(r, g), pd[4 * g], pd[4 * g + 1], pd[4 * g + 2], pd[4 * g + 3]);
-          tmem_st_wait();
+            for (int ch = 0; ch < 2; ++ch)
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                const float2 dl = *reinterpret_cast<const float2*>(&sm.delta[st][x * 64 + ch * 32 + e]);
+                float dpa = __uint_as_float(dr[ch][e]), dpb = __uint_as_float(dr[ch][e + 1]);
+                if (kDropout) {
+                  dpa = ((keep[ch] >> e) & 1u) ? dpa * prm.rp : 0.f;
+                  dpb = ((keep[ch] >> (e + 1)) & 1u) ? dpb * prm.rp : 0.f;
+                }
+                float da, db;
+                f2unpack(fmul2(f2pack(pf[ch * 32 + e], pf[ch * 32 + e + 1]), fadd2(f2pack(dpa, dpb), f2pack(-dl.x, -dl.y))),
+                         da, db);
+                pd[ch * 16 + e / 2] = pack_bf16(da, db);
+              }
+            if (warp_partial) {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) pd[e] = key_ok ? pd[e] : 0u;
+            }
+            tmem_st32(t_row + kColDP + x * 64, pd);       // dS^T: A operand of dK (TS)
+#pragma unroll
+            for (int g = 0; g < 8; ++g)                    // dS^T [key][query]: A operand of dQ (MN-major)
+              st_shared_v4(ds_addr + sw128_off(r, g), pd[4 * g], pd[4 * g + 1], pd[4 * g + 2], pd[4 * g + 3]);
+            tmem_st_wait();
+          }
           fence_proxy_async_smem();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.pds_full);
-          ++g_cnt;
+          if (lane == 0) mbar_arrive(&sm.ds_full);
           TR(7);
         }
       }
@@ -446,7 +527,8 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             asm volatile("prefetch.global.L1 [%0];" :: "l"(acc + 32) : "memory");
           }
           TR(30);
-          mbar_wait(&sm.dq_full, e_cnt & 1);
+          const uint32_t qb = e_cnt & 1;                    // this pair's dQ buffer
+          mbar_wait(&sm.dq_full[qb], (e_cnt >> 1) & 1);
           TR(31);
           tc_fence_after();
           if (i == it.nt - 1) {
@@ -495,12 +577,12 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             }
           }
           uint32_t d[64];
-          tmem_ld32(t_row + kColDQ, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
-          tmem_ld32(t_row + kColDQ + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
+          tmem_ld32(t_row + kColDQ + 64 * qb, *reinterpret_cast<uint32_t(*)[32]>(&d[0]));
+          tmem_ld32(t_row + kColDQ + 64 * qb + 32, *reinterpret_cast<uint32_t(*)[32]>(&d[32]));
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&sm.dq_empty);         // TMEM dQ free: the MMA may issue the next one
+          if (lane == 0) mbar_arrive(&sm.dq_empty[qb]);     // this TMEM dQ buffer is free again
           if (last) {
             // final: (partial +) this pass's part, x scale -> bf16 dQ
             if (!first && row_ok) {

@@ -1,6 +1,7 @@
-"""Correlate the bwd Q/dO producer with the MMA issuer in a trace build (CTA 0):
-per pair p, when the producer passed the stage-empty wait (23) and arrived (24), and when
-the MMA saw qdo_full (18), issued S (10/11) and finished issuing grads (19)."""
+"""Correlate the warps of CTA 0 in a bwd trace build, per pair p (cycles from kernel start):
+producer stage wait passed (23) / arrived (24); MMA: P_p seen + dV_p issue (12), S_{p+1}
+issued (10), dK_p/dQ_p/dP_{p+1} issued (19); compute warp 0: waiting (1), S_p in (2), exp done
+(3), P_p stored (4), dP_p in (5), dS_p stored (7); epilogue warp 8: dQ_p in (31), out (32)."""
 import ctypes as C, sys
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import numpy as np, torch
@@ -21,9 +22,10 @@ ev = (buf >> np.uint64(48)).astype(np.int64); ck = (buf & np.uint64(0xFFFFFFFFFF
 t0 = ck[ck > 0].min()
 def series(w, e):
     return [int(ck[w * 1024 + i] - t0) for i in range(1024) if buf[w * 1024 + i] and ev[w * 1024 + i] == e]
-p23, p24, m18, m10, m11, m19 = series(12, 23), series(12, 24), series(13, 18), series(13, 10), series(13, 11), series(13, 19)
-c2, c3, c4, c5, c7 = series(0, 2), series(0, 3), series(0, 4), series(0, 5), series(0, 7)
-print("pair  prodStage prodArrive  mmaQ  mmaSiss mmaSdone  cmpSgot cmpLd cmpMath cmpGradOk cmpStored  mmaGradsIssued(p-1)")
-for p in range(min(30, len(m18))):
-    g = lambda a: a[p] if p < len(a) else -1
-    print(f"{p:4d} {g(p23):9d} {g(p24):9d} {g(m18):7d} {g(m10):7d} {g(m11):8d} {g(c2):8d} {g(c3):6d} {g(c4):7d} {g(c5):8d} {g(c7):8d} {g(m19):8d}")
+cols = [("pSt", 12, 23), ("pArr", 12, 24), ("mP+dV", 13, 12), ("mS+1", 13, 10), ("mGr", 13, 19),
+        ("c1", 0, 1), ("cS", 0, 2), ("cExp", 0, 3), ("cP", 0, 4), ("cdP", 0, 5), ("cdS", 0, 7),
+        ("eQin", 8, 31), ("eQout", 8, 32)]
+ser = {n: series(w, e) for n, w, e in cols}
+print("pair " + " ".join(f"{n:>7s}" for n, _, _ in cols))
+for p in range(min(40, len(ser["cS"]))):
+    print(f"{p:4d} " + " ".join(f"{(ser[n][p] if p < len(ser[n]) else -1):7d}" for n, _, _ in cols))

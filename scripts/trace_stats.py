@@ -35,7 +35,7 @@ for w in range(nw):
     for (e0, c0), (e1, c1) in zip(row, row[1:]):
         st[(e0, e1)].append(c1 - c0)
     span = row[-1][1] - row[0][1]
-    parts = sorted(st.items(), key=lambda kv: -sum(kv[1]))[:10]
+    parts = sorted(st.items(), key=lambda kv: -sum(kv[1]))[:8]
     print(f"warp {w:2d} n={len(row)} first={row[0][1]} last={row[-1][1]} span={span}")
     for (a, b), v in parts:
         print(f"    {a:2d}->{b:2d} n={len(v):4d} mean={np.mean(v):8.0f} total={sum(v):8d} ({100*sum(v)/max(span,1):4.1f}%)")

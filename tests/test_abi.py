@@ -129,6 +129,47 @@ def test_balance_plan_lpt_bit_exact(ub):
         api.balance_plan_weighted([1, 2], 2, 1, 512, 0, 0)
 
 
+def test_balance_plan_stay_bit_exact(ub):
+    """UB_BAL_STAY vs oracle balance_stay (R25), bit-exact (perm, loads, send matrices)."""
+    from paper_2208_08124_b200 import api
+    rng = np.random.default_rng(13)
+    for W in (1, 2, 3, 8):
+        for B in (1, 2, 7, 56):
+            for trial in range(3):
+                a = rng.integers(1, 513, size=W * B).astype(np.int32) if trial < 2 else \
+                    synth.skewed_rank_lengths(W, B, trial, "iid").reshape(-1).astype(np.int32)
+                got = api.balance_plan(a, W, B, 512, "stay")
+                exp = obal.balance_stay(a, W, B)
+                for k in ("perm", "rank_tokens", "send_samples", "send_tokens"):
+                    assert np.array_equal(np.asarray(got[k], np.int64), np.asarray(exp[k], np.int64)), (W, B, k)
+
+
+def test_balance_relabel_locality_bit_exact(ub):
+    """ub_balance_relabel (DP over rank subsets) and the UB_BAL_LOCALITY flag vs the oracle's
+    exhaustive relabel_locality (R24), bit-exact, incl. ties (equal lengths everywhere)."""
+    from paper_2208_08124_b200 import api
+    rng = np.random.default_rng(9)
+    for W in (1, 2, 3, 5, 8):
+        for B in (1, 3, 56):
+            for trial in range(3):
+                a = (np.full(W * B, 7, np.int32) if trial == 2 else rng.integers(1, 513, size=W * B).astype(np.int32))
+                if trial == 1:
+                    a = synth.skewed_rank_lengths(W, B, 3, "sorted-block").reshape(-1).astype(np.int32)
+                for mode in ("paper", "snake", "lpt"):
+                    base = api.balance_plan(a, W, B, 512, mode)
+                    exp = obal.relabel_locality(a, base["perm"], W, B)
+                    got, kb, ka = api.balance_relabel(a, base["perm"], W, B)
+                    assert np.array_equal(got.astype(np.int64), exp), (W, B, mode)
+                    assert kb == obal.kept_tokens(a, base["perm"], W, B) and ka == obal.kept_tokens(a, exp, W, B)
+                    flag = api.balance_plan(a, W, B, 512, mode + "+locality")
+                    assert np.array_equal(flag["perm"].astype(np.int64), exp)
+                    assert sorted(flag["rank_tokens"].tolist()) == sorted(base["rank_tokens"].tolist())
+    from paper_2208_08124_b200 import UbError
+    with pytest.raises(UbError) as e:
+        api.balance_relabel(np.ones(4, np.int32), [0, 0, 1, 2], 2, 2)
+    assert e.value.status == 4
+
+
 def test_exchange_tables_reproduce_oracle_exchange(ub):
     """Apply the library's pack/unpack tables with plain numpy copies (the device kernel
     only follows the table) and compare the bytes every rank ends with to the oracle."""

@@ -196,3 +196,86 @@ def test_lpt_balances_far_better_at_8():
         imb_p.append(balance.imbalance(balance.balance_paper(a, 8, 56)["rank_tokens"]))
         imb_l.append(balance.imbalance(balance.balance_lpt(a, 8, 56)["rank_tokens"]))
     assert np.mean(imb_l) < 0.002 < np.mean(imb_p)
+
+
+# ---------------------------------------------------------------- locality relabeling (R24, NEXT-2)
+def test_relabel_locality_hand_worked():
+    """W=2, B=2, lengths rank0 = [5, 1], rank1 = [2, 9] (ids 0..3).  Paper plan: sorted
+    ids by length = [1(1), 2(2), 0(5), 3(9)]; rank0 <- [1, 0], rank1 <- [2, 3].  Group 0
+    = {1, 0} is all rank-0 data (6 tokens), group 1 = {2, 3} all rank-1 data (11): the
+    identity labeling keeps all 17 tokens, the swap keeps 0 -> identity stays."""
+    a = [5, 1, 2, 9]
+    plan = balance.balance_paper(a, 2, 2)
+    assert plan["perm"].tolist() == [1, 0, 2, 3]
+    assert balance.relabel_locality(a, plan["perm"], 2, 2).tolist() == [1, 0, 2, 3]
+    assert balance.kept_tokens(a, plan["perm"], 2, 2) == 17
+    # rank0 = [9, 2], rank1 = [1, 5]: sorted [2(1), 1(2), 3(5), 0(9)] -> group0 {2, 3} (rank-1
+    # data, 6), group1 {1, 0} (rank-0 data, 11): identity keeps 0, the swap keeps 17
+    a = [9, 2, 1, 5]
+    plan = balance.balance_paper(a, 2, 2)
+    assert plan["perm"].tolist() == [2, 3, 1, 0]
+    assert balance.kept_tokens(a, plan["perm"], 2, 2) == 0
+    r = balance.relabel_locality(a, plan["perm"], 2, 2)
+    assert r.tolist() == [1, 0, 2, 3] and balance.kept_tokens(a, r, 2, 2) == 17
+
+
+@pytest.mark.parametrize("W", [2, 3, 4, 5, 6])
+def test_relabel_locality_vs_hungarian_and_invariants(W):
+    from scipy.optimize import linear_sum_assignment
+    for seed in range(12):
+        B = 7
+        a = synth.skewed_rank_lengths(W, B, seed, "iid" if seed % 2 else "sorted-block").reshape(-1)
+        for mode in ("paper", "snake", "lpt"):
+            plan = {"paper": balance.balance_paper, "snake": balance.balance_snake,
+                    "lpt": balance.balance_lpt}[mode](a, W, B)
+            perm = plan["perm"]
+            r = balance.relabel_locality(a, perm, W, B)
+            # the optimum of the assignment problem, by an independent routine
+            M = np.zeros((W, W))
+            for i in range(W):
+                for k in range(B):
+                    g = int(perm[i * B + k])
+                    M[i, g // B] += a[g]
+            rows, cols = linear_sum_assignment(M, maximize=True)
+            assert balance.kept_tokens(a, r, W, B) == int(M[rows, cols].sum())
+            assert balance.kept_tokens(a, r, W, B) >= balance.kept_tokens(a, perm, W, B)
+            # every group survives intact (same ids, same order), only its rank changes
+            groups = sorted(tuple(int(x) for x in perm[i * B:(i + 1) * B]) for i in range(W))
+            assert sorted(tuple(int(x) for x in r[i * B:(i + 1) * B]) for i in range(W)) == groups
+            assert sorted(balance.plan_from_groups(a, W, B, [list(r[i * B:(i + 1) * B]) for i in range(W)])
+                          ["rank_tokens"].tolist()) == sorted(plan["rank_tokens"].tolist())
+
+
+# ---------------------------------------------------------------- stay-home balancing (R25, NEXT-2)
+def test_balance_stay_hand_worked():
+    """W=2, B=2: rank0 = [10, 2] (ids 0, 1), rank1 = [1, 3] (ids 2, 3); loads 12 / 4.
+    Pairs x in rank0, y in rank1 with d > 0: (0,2) d=9 -> max(3, 13) = 13; (0,3) d=7 ->
+    max(5, 11) = 11; (1,2) d=1 -> max(11, 5) = 11.  Best value 11, tie (0,3) vs (1,2) ->
+    (0,3) first.  11 < 12: swap -> rank0 {3, 1} = 5, rank1 {2, 0} = 11.  Next: M = rank1,
+    m = rank0: pairs x in {2, 0}, y in {3, 1}: (0,3) d=7 -> max(4, 12); (0,1) d=8 -> max(3,
+    13); none beats 11.  Stop.  Sorted: rank0 [1 (2), 3 (3)], rank1 [2 (1), 0 (10)]."""
+    p = balance.balance_stay([10, 2, 1, 3], 2, 2)
+    assert p["perm"].tolist() == [1, 3, 2, 0]
+    assert p["rank_tokens"].tolist() == [5, 11]
+
+
+def test_balance_stay_invariants():
+    for W in (1, 2, 3, 8):
+        for seed in range(6):
+            B = 56 if W == 8 else 9
+            a = synth.skewed_rank_lengths(W, B, seed, "iid").reshape(-1)
+            p = balance.balance_stay(a, W, B)
+            perm = [int(x) for x in p["perm"]]
+            assert sorted(perm) == list(range(W * B))                        # a permutation
+            before = [int(a[r * B:(r + 1) * B].sum()) for r in range(W)]
+            assert max(p["rank_tokens"]) <= max(before)                      # never worse than not moving
+            moved = [g for r in range(W) for g in perm[r * B:(r + 1) * B] if g // B != r]
+            assert len(moved) % 2 == 0 or W > 2                              # swaps move samples in pairs
+            for r in range(W):                                               # rank order: (length, id)
+                blk = perm[r * B:(r + 1) * B]
+                assert blk == sorted(blk, key=lambda g: (a[g], g))
+            if W == 1:
+                assert moved == []
+    # all lengths equal: nothing to balance, nothing moves
+    p = balance.balance_stay([5] * 12, 3, 4)
+    assert all(int(g) // 4 == r for r in range(3) for g in p["perm"][r * 4:(r + 1) * 4])
