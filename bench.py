@@ -54,8 +54,8 @@ H, D, S, B = 16, 64, 512, 56
 REC = 16      # per-token record: input_id, segment_id, masked_lm_label, position (int32 x 4)
 SREC = 4      # per-sample record: next_sentence_label (int32)
 N_SETS = 3    # rotating input sets: each step's working set (> 300 MB) and the 2 others exceed L2
-N_EX = 4      # exchange output buffers in flight: the side stream never waits on the step just enqueued
-PIPE = 2      # step n computes while step n+PIPE is exchanged and n+PIPE+1's lengths are gathered
+N_EX = 5      # exchange output buffers in flight: the side stream never waits on the step just enqueued
+PIPE = 3      # step n computes while step n+PIPE is exchanged and n+PIPE+1's lengths are gathered
 KERNELS_PER_STEP = 6    # ours: unpad, 2x exchange copy, fwd main (+ fused pad), bwd pre (Delta) + main
 
 
@@ -364,10 +364,16 @@ class Workload:
                     "cu": torch.empty(B + 1, dtype=torch.int32, device=dev), "T": 0, "L": None} for _ in range(N_EX)]
         self.out = torch.empty((self.cap, H, D), dtype=torch.bfloat16, device=dev)
         self.lse = torch.empty((H, self.cap), dtype=torch.float32, device=dev)
+        self.lse_buf = self.lse                               # the hot loop's [H, T] view of the same memory
+        self._begin, self._finish, self._unpad, self._fmha, self._prof_on = {}, {}, {}, {}, False
         self.dqkv = torch.empty((self.cap, 3, H, D), dtype=torch.bfloat16, device=dev)
         self.padded_out = torch.empty((B, S, H, D), dtype=torch.bfloat16, device=dev)
-        self.main = torch.cuda.current_stream()
-        self.side = torch.cuda.Stream()
+        # the compute stream at the highest priority, the exchange at the lowest: when an SM
+        # frees up between two persistent FMHA kernels the block scheduler hands it to the
+        # compute stream, so side-stream copies never delay a persistent grid's start
+        self.main = torch.cuda.Stream(priority=-5)
+        torch.cuda.set_stream(self.main)
+        self.side = torch.cuda.Stream(priority=0)
         self.ex_ready = [torch.cuda.Event() for _ in range(N_EX)]
         self.done = [torch.cuda.Event() for _ in range(N_EX)]
         self.comm = ub.Comm(world, rank)
@@ -381,27 +387,45 @@ class Workload:
 
     def begin(self, n):
         """Side stream, two steps ahead: a1 all-gather of step n's lengths (no host wait)."""
-        st = self.sets[n % N_SETS]
-        self.comm.exchange_begin(n % self.comm.SLOTS, st["lengths"], self.cap, REC, SREC, stream=self.side)
+        key = (n % self.comm.SLOTS, n % N_SETS)
+        f = self._begin.get(key)
+        if f is None:
+            st = self.sets[n % N_SETS]
+            f = self._begin[key] = self.comm.bind_begin(key[0], st["lengths"], self.cap, REC, SREC, stream=self.side)
+        f()
 
     def finish(self, n, marks=None):
         """Side stream, one step ahead: a6 unpad of step n's input records, a2-a5 plan and
         exchange.  Its one host wait is for the lengths begin(n) fetched a step earlier."""
-        st, ex = self.sets[n % N_SETS], self.ex[n % N_EX]
-        self.side.wait_event(self.done[n % N_EX])         # step n-N_EX finished with these buffers
-        self.ub.unpad(st["padded_recs"], st["cu_local"], st["T"], out=self.packed_recs[:st["T"]],
-                      stream=self.side)
+        s, e = n % N_SETS, n % N_EX
+        st, ex = self.sets[s], self.ex[e]
+        self.side.wait_event(self.done[e])                # step n-N_EX finished with these buffers
+        u = self._unpad.get(s)
+        if u is None:
+            u = self._unpad[s] = self.ub.api.BoundUnpad(st["padded_recs"], st["cu_local"], self.packed_recs,
+                                                        stream=self.side)
+        u(st["T"])
         if marks is not None:
             marks.append(time.perf_counter())
-        T, perm = self.comm.exchange_finish(n % self.comm.SLOTS, B, self.packed_recs[:st["T"]], st["samples"],
-                                            self.cap, S, self.args.balance, ex["tokens"], ex["samples"], ex["cu"],
-                                            stream=self.side)
-        allL = np.asarray(self.all_lengths_cache(n), np.int64)
+        key = (n % self.comm.SLOTS, s, e)
+        f = self._finish.get(key)
+        if f is None:
+            f = self._finish[key] = self.comm.bind_finish(key[0], B, self.packed_recs, st["samples"], self.cap, S,
+                                                          self.args.balance, ex["tokens"], ex["samples"], ex["cu"],
+                                                          stream=self.side)
+        T, perm = f()
         ex["T"] = T
-        ex["L"] = allL[perm[self.rank * B:(self.rank + 1) * B]]
-        self.ex_ready[n % N_EX].record(self.side)
+        ex["perm"] = perm.copy()
+        self.ex_ready[e].record(self.side)
         if marks is not None:
             marks.append(time.perf_counter())
+
+    def lens_of(self, n):
+        """Lengths of this rank's post-exchange batch of step n (host bookkeeping, outside the
+        timed enqueue)."""
+        ex = self.ex[n % N_EX]
+        allL = np.asarray(self.all_lengths_cache(n), np.int64)
+        return allL[ex["perm"][self.rank * B:(self.rank + 1) * B]]
 
     def all_lengths_cache(self, n):
         s = n % N_SETS
@@ -411,35 +435,40 @@ class Workload:
             self._all_l[s] = synth.skewed_rank_lengths(self.world, B, s, self.args.skew, self.args.dist).reshape(-1)
         return self._all_l[s]
 
-    def view(self, owner, key, T):
-        """owner[key][:T], cached (slicing a tensor costs ~1.5 us of host time)."""
-        d = owner.setdefault("_views", {}) if isinstance(owner, dict) else self.__dict__.setdefault("_views", {})
-        k = (key, T, id(owner[key] if isinstance(owner, dict) else getattr(owner, key)))
-        v = d.get(k)
-        if v is None:
-            v = d[k] = (owner[key] if isinstance(owner, dict) else getattr(owner, key))[:T]
-        return v
+    def bound(self, n):
+        """The pre-marshalled FMHA calls of step n's buffers (input set, exchange slot, dqkv)."""
+        s, e = n % N_SETS, n % N_EX
+        key = (s, e, self.dqkv.data_ptr())
+        b = self._fmha.get(key)
+        if b is None:
+            st = self.sets[s]
+            b = self._fmha[key] = self.ub.api.BoundFmha(
+                st["qkv"], self.ex[e]["cu"], S, self.out, self.lse_buf, dout=st["dout"], dqkv=self.dqkv,
+                p_dropout=self.args.p_dropout, stream=self.main, num_ctas=self.ctas, padded=self.padded_out)
+        return b
 
     def step(self, n, prof=None, marks=None):
-        """Main stream: a7 fwd, a8 bwd, a9 pad for step n.  marks: host timestamps."""
-        st, ex = self.sets[n % N_SETS], self.ex[n % N_EX]
+        """Main stream: a7 fwd (+ fused a9 pad), a8 bwd for step n.  marks: host timestamps."""
+        ex = self.ex[n % N_EX]
         T = ex["T"]
         self.main.wait_event(self.ex_ready[n % N_EX])
-        p = self.args.p_dropout
         if prof is not None:
             for kid, pair in prof.items():
                 self.ub.api.profile_events(kid, *pair)
+            self._prof_on = True
+        elif self._prof_on:                                 # unregister: this step runs uninstrumented
+            for kid in (0, 1, 3):
+                self.ub.api.profile_events(kid)
+            self._prof_on = False
         if marks is not None:
             marks.append(time.perf_counter())
-        qkv, out = self.view(st, "qkv", T), self.view(self, "out", T)
+        b = self.bound(n)
         # a7 + a9: the forward's epilogue also writes the padded copy of O (P:318), zeros past
         # each length -- the separate pad pass is gone (ub_varlen_fmha_fwd_pad)
-        self.ub.varlen_fmha_fwd(qkv, ex["cu"], S, None, p, 0x2208 + n, 0, out=out, lse=self.lse, num_ctas=self.ctas,
-                                stream=self.main, padded=self.padded_out)
+        b.fwd(T, 0x2208 + n)
         if marks is not None:
             marks.append(time.perf_counter())
-        self.ub.varlen_fmha_bwd(qkv, out, self.lse, self.view(st, "dout", T), ex["cu"], S, None, p, 0x2208 + n, 0,
-                                dqkv=self.view(self, "dqkv", T), num_ctas=self.ctas, stream=self.main)
+        b.bwd(T, 0x2208 + n)
         if marks is not None:
             marks.append(time.perf_counter())
         self.done[n % N_EX].record(self.main)
@@ -460,7 +489,6 @@ def run_ours(args, world, rank, local):
     for n in range(PIPE):
         wl.finish(n)
     for n in range(args.warmup):
-        _patch_lse(wl, n)
         wl.step(n)
         wl.finish(n + PIPE)
         wl.begin(n + PIPE + 1)
@@ -488,14 +516,10 @@ def run_ours(args, world, rank, local):
         n = args.warmup + k
         step_ev[k].record(wl.main)
         h0 = time.perf_counter()
-        _patch_lse(wl, n)
         m = []
         profiled = k % args.prof_every == 0
-        if not profiled:                  # unregister the events so this step runs uninstrumented
-            for kid in kids:
-                ub.api.profile_events(kid)
         tokens += wl.step(n, prof_events[k] if profiled else None, m)
-        lens_used.append(wl.ex[n % N_EX]["L"])
+        lens_used.append((n, wl.ex[n % N_EX]["perm"]))      # a reference; lengths derived after the loop
         h1 = time.perf_counter()
         wl.finish(n + PIPE, m)
         wl.begin(n + PIPE + 1)
@@ -511,6 +535,8 @@ def run_ours(args, world, rank, local):
     clk = clocks.stop()
     for kid in kids:
         ub.api.profile_events(kid)
+    wl._prof_on = False
+    lens_used = [np.asarray(wl.all_lengths_cache(nn), np.int64)[pp[rank * B:(rank + 1) * B]] for nn, pp in lens_used]
     last = args.warmup + args.steps + PIPE
     wl.finish(last)                   # drain the begin still in flight (untimed)
     torch.cuda.synchronize()
@@ -609,13 +635,10 @@ def exchange_overlap(args, wl, world, last, step_us):
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for k in range(3):
-        _patch_lse(wl, done[k % N_EX])
         wl.step(done[k % N_EX])
     e0.record(wl.main)
     for k in range(K):
-        n = done[k % N_EX]
-        _patch_lse(wl, n)
-        wl.step(n)
+        wl.step(done[k % N_EX])
     e1.record(wl.main)
     torch.cuda.synchronize()
     comp = all_max(e0.elapsed_time(e1), world) / K * 1e3

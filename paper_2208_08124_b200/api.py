@@ -161,6 +161,74 @@ def varlen_fmha_bwd(qkv, out, lse, dout, cu, max_seqlen: int, scale=None, p_drop
     return dqkv
 
 
+# ------------------------------------------------------------------ pre-marshalled calls (hot loops)
+class BoundFmha:
+    """The varlen FMHA forward (+ fused pad) and backward on fixed buffers, with every pointer,
+    the stream and the parameter struct marshalled once: a call only updates T (and the
+    dropout seed) and invokes the C entry point.  Same ABI calls as varlen_fmha_fwd / _bwd --
+    argument marshalling hoisted out of a training loop whose buffers do not change.
+    qkv / dout / out / dqkv: capacity-sized tensors whose first T rows are used; lse: a buffer
+    of at least H * T floats, used as a dense [H, T] array."""
+
+    def __init__(self, qkv, cu, max_seqlen, out, lse, dout=None, dqkv=None, scale=None, p_dropout=0.0, seed=0,
+                 offset=0, stream=None, num_ctas=0, padded=None):
+        cap, three, H, D = qkv.shape
+        B = cu.numel() - 1
+        self.prm = fmha_params(B, cap, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas)
+        self._p = C.byref(self.prm)
+        L = lib()
+        ws_f = _workspace(L.ub_fmha_workspace_bytes(self._p, 0), qkv.device, "fmha_fwd")
+        ws_b = _workspace(L.ub_fmha_workspace_bytes(self._p, 1), qkv.device, "fmha_bwd")
+        self._keep = (qkv, cu, out, lse, dout, dqkv, padded, ws_f, ws_b)   # keep the buffers alive
+        st = _stream(stream)
+        if padded is not None:
+            self._fwd = L.ub_varlen_fmha_fwd_pad
+            self._fwd_args = (self._p, _ptr(qkv), _ptr(cu), _ptr(out), _ptr(lse), _ptr(padded), int(padded.shape[1]),
+                              _ptr(ws_f), st)
+        else:
+            self._fwd = L.ub_varlen_fmha_fwd
+            self._fwd_args = (self._p, _ptr(qkv), _ptr(cu), _ptr(out), _ptr(lse), _ptr(ws_f), st)
+        self._bwd = L.ub_varlen_fmha_bwd
+        self._bwd_args = (self._p, _ptr(qkv), _ptr(out), _ptr(lse), _ptr(dout), _ptr(cu), _ptr(dqkv), _ptr(ws_b), st)
+        self.cap = cap
+
+    def _set(self, T, seed):
+        assert 0 < T <= self.cap
+        self.prm.T = T
+        if seed is not None:
+            self.prm.seed = seed
+
+    def fwd(self, T: int, seed=None):
+        self._set(T, seed)
+        st = self._fwd(*self._fwd_args)
+        if st:
+            check(st)
+
+    def bwd(self, T: int, seed=None):
+        self._set(T, seed)
+        st = self._bwd(*self._bwd_args)
+        if st:
+            check(st)
+
+
+class BoundUnpad:
+    """ub_unpad on fixed buffers (padded [B, S, *row] -> out), marshalled once; call with T."""
+
+    def __init__(self, padded, cu, out, stream=None):
+        self._keep = (padded, cu, out)
+        B, S = padded.shape[0], padded.shape[1]
+        row = padded[0, 0].numel() * padded.element_size()
+        self._args = [_ptr(padded), _ptr(out), _ptr(cu), B, S, 0, row, _stream(stream)]
+        self._f = lib().ub_unpad
+
+    def __call__(self, T: int):
+        a = self._args
+        a[5] = int(T)
+        st = self._f(*a)
+        if st:
+            check(st)
+
+
 # ------------------------------------------------------------------ Dropout_Add_LayerNorm
 def dal_fwd(a: torch.Tensor, res: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor, p_dropout=0.0, eps=1e-12,
             seed=0, offset=0, out=None, mean=None, rstd=None, stream=None):
@@ -479,6 +547,42 @@ class Comm:
                                        _ptr(out_samples), _ptr(out_cu), _np_ptr(perm), C.byref(T_out), _ptr(ws),
                                        _stream(stream)))
         return int(T_out.value), perm
+
+    def bind_finish(self, slot: int, B, d_tokens, d_samples, capacity_tokens, max_seqlen, mode, out_tokens,
+                    out_samples, out_cu, stream=None):
+        """exchange_finish on fixed buffers, marshalled once: returns a callable () -> (T_out,
+        perm) (perm: this binding's own int32 array, overwritten by the next call)."""
+        rec = int(np.prod(d_tokens.shape[1:])) * d_tokens.element_size()
+        srec = int(np.prod(d_samples.shape[1:])) * d_samples.element_size() if d_samples is not None else 0
+        ws = self._ws(B, capacity_tokens, rec, srec, out_tokens.device)
+        perm = np.zeros(self.world * B, dtype=np.int32)
+        T_out = C.c_int64(0)
+        args = (self.handle, int(slot), _mode(mode), B, int(max_seqlen), _ptr(d_tokens), _ptr(d_samples), rec, srec,
+                int(capacity_tokens), _ptr(out_tokens), _ptr(out_samples), _ptr(out_cu), _np_ptr(perm), C.byref(T_out),
+                _ptr(ws), _stream(stream))
+        f = lib().ub_exchange_finish
+        keep = (d_tokens, d_samples, out_tokens, out_samples, out_cu, ws)
+
+        def call():
+            st = f(*args)
+            if st:
+                check(st)
+            return T_out.value, perm
+        call.keep = keep
+        return call
+
+    def bind_begin(self, slot: int, d_lengths, capacity_tokens, rec, srec, stream=None):
+        """exchange_begin marshalled once: returns a callable ()."""
+        ws = self._ws(d_lengths.numel(), capacity_tokens, rec, srec, d_lengths.device)
+        args = (self.handle, int(slot), d_lengths.numel(), _ptr(d_lengths), _ptr(ws), _stream(stream))
+        f = lib().ub_exchange_begin
+
+        def call():
+            st = f(*args)
+            if st:
+                check(st)
+        call.keep = (d_lengths, ws)
+        return call
 
     def close(self):
         if self.handle:

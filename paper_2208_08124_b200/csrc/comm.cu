@@ -27,9 +27,7 @@ struct Comm {
   // and guarded by ev_len[slot].  The plan tables / cu are rewritten by every finish only
   // after ev_staging (behind the previous finish's H2D copies) has fired.
   int32_t* h_all = nullptr;
-  int64_t* h_tab_pack = nullptr;
-  int64_t* h_tab_unpack = nullptr;
-  int32_t* h_cu = nullptr;
+  int64_t* h_stage = nullptr;         // tables + new cu_seqlens, one H2D per finish (stage_words(B) int64)
   int32_t cap_B = 0;
   int32_t slot_B[kExSlots] = {};      // B of the pending begin, 0 = free
   cudaEvent_t ev_len[kExSlots] = {};
@@ -56,12 +54,13 @@ static double now_us() {
       return ::ub::set_error(UB_ERR_NCCL, "%s: %s", #expr, ncclGetErrorString(r_));          \
   } while (0)
 
+// staged per finish: pack table [5B] | gather table [6B] | new cu_seqlens [B+1] int32 (padded to int64)
+static size_t stage_words(int32_t B) { return (size_t)11 * B + ((size_t)B + 2) / 2; }
+
 static void free_staging(Comm* c) {
   cudaFreeHost(c->h_all);
-  cudaFreeHost(c->h_tab_pack);
-  cudaFreeHost(c->h_tab_unpack);
-  cudaFreeHost(c->h_cu);
-  c->h_all = nullptr; c->h_tab_pack = nullptr; c->h_tab_unpack = nullptr; c->h_cu = nullptr; c->cap_B = 0;
+  cudaFreeHost(c->h_stage);
+  c->h_all = nullptr; c->h_stage = nullptr; c->cap_B = 0;
 }
 
 static ub_status ensure_staging(Comm* c, int32_t B) {
@@ -78,9 +77,7 @@ static ub_status ensure_staging(Comm* c, int32_t B) {
   c->h_all = nullptr;
   free_staging(c);
   UB_CHECK_CUDA(cudaMallocHost(&c->h_all, sizeof(int32_t) * (size_t)kExSlots * c->W * B));
-  UB_CHECK_CUDA(cudaMallocHost(&c->h_tab_pack, sizeof(int64_t) * 5 * (size_t)B));
-  UB_CHECK_CUDA(cudaMallocHost(&c->h_tab_unpack, sizeof(int64_t) * 5 * (size_t)B));
-  UB_CHECK_CUDA(cudaMallocHost(&c->h_cu, sizeof(int32_t) * ((size_t)B + 1)));
+  UB_CHECK_CUDA(cudaMallocHost(&c->h_stage, sizeof(int64_t) * stage_words(B)));
   if (old_all) {
     for (int32_t k = 0; k < kExSlots; ++k)
       if (c->slot_B[k])
@@ -93,15 +90,14 @@ static ub_status ensure_staging(Comm* c, int32_t B) {
 }
 
 struct ExWs {  // carve-up of the exchange workspace
-  int32_t* all_lengths; int64_t* tab_pack; int64_t* tab_unpack;
+  int32_t* all_lengths; int64_t* stage;
   uint8_t* send_tok; uint8_t* recv_tok; uint8_t* send_smp; uint8_t* recv_smp;
 };
 static size_t ex_layout(int32_t W, int32_t B, int64_t cap, int64_t rec, int64_t srec, void* base, ExWs* out) {
   size_t off = 0;
   auto take = [&](size_t n) { size_t o = off; off = align_up(off + n, 256); return o; };
   const size_t o_all = take(sizeof(int32_t) * (size_t)kExSlots * W * B);  // one gather target per slot
-  const size_t o_tp = take(sizeof(int64_t) * 5 * (size_t)B);
-  const size_t o_tu = take(sizeof(int64_t) * 5 * (size_t)B);
+  const size_t o_tp = take(sizeof(int64_t) * stage_words(B));
   const size_t o_st = take((size_t)cap * rec);
   const size_t o_rt = take((size_t)cap * rec);
   const size_t o_ss = take((size_t)B * srec);
@@ -109,8 +105,7 @@ static size_t ex_layout(int32_t W, int32_t B, int64_t cap, int64_t rec, int64_t 
   if (out && base) {
     char* b = static_cast<char*>(base);
     out->all_lengths = reinterpret_cast<int32_t*>(b + o_all);
-    out->tab_pack = reinterpret_cast<int64_t*>(b + o_tp);
-    out->tab_unpack = reinterpret_cast<int64_t*>(b + o_tu);
+    out->stage = reinterpret_cast<int64_t*>(b + o_tp);
     out->send_tok = reinterpret_cast<uint8_t*>(b + o_st);
     out->recv_tok = reinterpret_cast<uint8_t*>(b + o_rt);
     out->send_smp = reinterpret_cast<uint8_t*>(b + o_ss);
@@ -254,79 +249,97 @@ static ub_status exchange_finish(Comm* c, int32_t slot, int32_t mode, int32_t B,
   // the previous finish's H2D copies out of the staging buffers must have completed
   UB_CHECK_CUDA(cudaEventSynchronize(c->ev_staging));
   UB_PHASE();
-  std::vector<int64_t> send_cnt(W), send_scnt(W), recv_cnt(W), recv_scnt(W);
-  int64_t T_mine = 0, T_out = 0;
-  if ((st = ub_exchange_tables(h_all, perm.data(), W, B, me, 0, c->h_tab_pack, send_cnt.data(), send_scnt.data(),
-                               &T_mine)) != UB_OK)
-    return st;
-  if ((st = ub_exchange_tables(h_all, perm.data(), W, B, me, 1, c->h_tab_unpack, recv_cnt.data(), recv_scnt.data(),
-                               &T_out)) != UB_OK)
-    return st;
-  UB_REQUIRE(T_mine <= cap && T_out <= cap, UB_ERR_CAPACITY, "tokens (%lld sent, %lld received) exceed capacity %lld",
-             (long long)T_mine, (long long)T_out, (long long)cap);
-  UB_PHASE();
-  // 4. pack into destination order
-  UB_CHECK_CUDA(cudaMemcpyAsync(w.tab_pack, c->h_tab_pack, sizeof(int64_t) * 5 * B, cudaMemcpyHostToDevice, s));
-  UB_CHECK_CUDA(cudaMemcpyAsync(w.tab_unpack, c->h_tab_unpack, sizeof(int64_t) * 5 * B, cudaMemcpyHostToDevice, s));
-  if ((st = ub_exchange_copy(d_my_tokens, w.send_tok, d_my_samples, w.send_smp, w.tab_pack, B, rec, srec, s)) != UB_OK)
-    return st;
-  UB_PHASE();
-  // 5. all-to-all-v over NVLink (grouped point-to-point); the chunk a rank keeps is a
-  // device copy, so one rank issues no collective at all (unless force_nccl: then the self
-  // chunk is an ncclSend/ncclRecv pair to itself inside the same group)
-  int64_t so = 0, ro = 0, sso = 0, rso = 0;
-  bool any_peer = false;
+  std::vector<int64_t> send_cnt(W, 0), send_scnt(W, 0), recv_cnt(W, 0), recv_scnt(W, 0);
   const bool self_nccl = c->force_nccl;
-  for (int32_t peer = 0; peer < W; ++peer) {
-    if (peer == me && self_nccl) {
-      UB_REQUIRE(send_cnt[me] == recv_cnt[me] && send_scnt[me] == recv_scnt[me], UB_ERR_INVALID_ARG,
-                 "exchange tables disagree on the self chunk");
-      any_peer = any_peer || send_cnt[me] > 0 || send_scnt[me] > 0;
-    } else if (peer == me) {
-      UB_REQUIRE(send_cnt[me] == recv_cnt[me] && send_scnt[me] == recv_scnt[me], UB_ERR_INVALID_ARG,
-                 "exchange tables disagree on the self chunk");
-      if (send_cnt[me] > 0)
-        UB_CHECK_CUDA(cudaMemcpyAsync(w.recv_tok + ro * rec, w.send_tok + so * rec, (size_t)(send_cnt[me] * rec),
-                                      cudaMemcpyDeviceToDevice, s));
-      if (srec > 0 && send_scnt[me] > 0)
-        UB_CHECK_CUDA(cudaMemcpyAsync(w.recv_smp + rso * srec, w.send_smp + sso * srec,
-                                      (size_t)(send_scnt[me] * srec), cudaMemcpyDeviceToDevice, s));
-    } else {
-      any_peer = any_peer || send_cnt[peer] > 0 || recv_cnt[peer] > 0 || send_scnt[peer] > 0 || recv_scnt[peer] > 0;
+  int64_t* hp = c->h_stage;                               // pack table, stride B
+  int64_t* hu = c->h_stage + (size_t)5 * B;               // gather table, stride B, 6 rows
+  int32_t* hcu = reinterpret_cast<int32_t*>(c->h_stage + (size_t)11 * B);
+  int32_t n_pack = 0;
+  int64_t T_out = 0;
+  {
+    // this rank's local cu_seqlens
+    std::vector<int64_t> cu((size_t)B + 1, 0);
+    for (int32_t k = 0; k < B; ++k) cu[k + 1] = cu[k] + h_all[(size_t)me * B + k];
+    // pack: the samples of this rank that other ranks take, by destination, each in its perm
+    // order (the part a rank keeps is read straight from its own buffer by the gather below,
+    // unless force_nccl sends it to itself)
+    int64_t off = 0;
+    for (int32_t dst = 0; dst < W; ++dst) {
+      if (dst == me && !self_nccl) continue;
+      for (int32_t k = 0; k < B; ++k) {
+        const int32_t g = perm[(size_t)dst * B + k];
+        if (g / B != me) continue;
+        hp[n_pack] = cu[g % B]; hp[B + n_pack] = h_all[g]; hp[2 * B + n_pack] = off;
+        hp[3 * B + n_pack] = g % B; hp[4 * B + n_pack] = n_pack;
+        off += h_all[g]; send_cnt[dst] += h_all[g]; send_scnt[dst] += 1; ++n_pack;
+      }
     }
-    so += send_cnt[peer]; ro += recv_cnt[peer]; sso += send_scnt[peer]; rso += recv_scnt[peer];
+    UB_REQUIRE(off <= cap, UB_ERR_CAPACITY, "tokens sent (%lld) exceed capacity %lld", (long long)off, (long long)cap);
+    // gather: output sample k (perm order) from this rank's buffer (sel 0) or from its source
+    // rank's chunk of the receive buffer (sel 1, chunks by source rank ascending)
+    for (int32_t k = 0; k < B; ++k) {
+      const int32_t g = perm[(size_t)me * B + k], src = g / B;
+      if (src == me && !self_nccl) continue;
+      recv_cnt[src] += h_all[g];
+      recv_scnt[src] += 1;
+    }
+    std::vector<int64_t> base(W, 0), sbase(W, 0);
+    for (int32_t q = 1; q < W; ++q) { base[q] = base[q - 1] + recv_cnt[q - 1]; sbase[q] = sbase[q - 1] + recv_scnt[q - 1]; }
+    hcu[0] = 0;
+    for (int32_t k = 0; k < B; ++k) {
+      const int32_t g = perm[(size_t)me * B + k], src = g / B;
+      if (src == me && !self_nccl) {
+        hu[k] = cu[g % B]; hu[3 * B + k] = g % B; hu[5 * B + k] = 0;
+      } else {
+        hu[k] = base[src]; hu[3 * B + k] = sbase[src]; hu[5 * B + k] = 1;
+        base[src] += h_all[g]; sbase[src] += 1;
+      }
+      hu[B + k] = h_all[g]; hu[2 * B + k] = T_out; hu[4 * B + k] = k;
+      T_out += h_all[g];
+      UB_REQUIRE(T_out <= INT32_MAX, UB_ERR_SHAPE, "received tokens overflow int32");
+      hcu[k + 1] = (int32_t)T_out;
+    }
+    UB_REQUIRE(T_out <= cap, UB_ERR_CAPACITY, "tokens received (%lld) exceed capacity %lld", (long long)T_out,
+               (long long)cap);
   }
+  UB_PHASE();
+  // 4. one H2D of both tables and the new cu_seqlens; pack what leaves this rank
+  UB_CHECK_CUDA(cudaMemcpyAsync(w.stage, c->h_stage, sizeof(int64_t) * stage_words(B), cudaMemcpyHostToDevice, s));
+  if (n_pack > 0 &&
+      (st = exchange_gather(d_my_tokens, nullptr, w.send_tok, d_my_samples, nullptr, w.send_smp, w.stage, nullptr, n_pack,
+                            B, rec, srec, nullptr, nullptr, 0, s)) != UB_OK)
+    return st;
+  UB_PHASE();
+  // 5. all-to-all-v over NVLink (grouped point-to-point; the self chunk only with force_nccl)
+  bool any_peer = false;
+  for (int32_t peer = 0; peer < W; ++peer)
+    any_peer = any_peer || send_cnt[peer] > 0 || recv_cnt[peer] > 0 || send_scnt[peer] > 0 || recv_scnt[peer] > 0;
   if (any_peer) {
     UB_CHECK_NCCL(ncclGroupStart());
-    so = ro = sso = rso = 0;
+    int64_t so = 0, ro = 0, sso = 0, rso = 0;
     for (int32_t peer = 0; peer < W; ++peer) {
-      if (peer != me || self_nccl) {
-        if (send_cnt[peer] > 0)
-          UB_CHECK_NCCL(ncclSend(w.send_tok + so * rec, (size_t)(send_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
-        if (recv_cnt[peer] > 0)
-          UB_CHECK_NCCL(ncclRecv(w.recv_tok + ro * rec, (size_t)(recv_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
-        if (srec > 0 && send_scnt[peer] > 0)
-          UB_CHECK_NCCL(
-              ncclSend(w.send_smp + sso * srec, (size_t)(send_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
-        if (srec > 0 && recv_scnt[peer] > 0)
-          UB_CHECK_NCCL(
-              ncclRecv(w.recv_smp + rso * srec, (size_t)(recv_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
-        c->nccl_ops += (send_cnt[peer] > 0) + (recv_cnt[peer] > 0) + (srec > 0 && send_scnt[peer] > 0) +
-                       (srec > 0 && recv_scnt[peer] > 0);
-      }
+      if (send_cnt[peer] > 0)
+        UB_CHECK_NCCL(ncclSend(w.send_tok + so * rec, (size_t)(send_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
+      if (recv_cnt[peer] > 0)
+        UB_CHECK_NCCL(ncclRecv(w.recv_tok + ro * rec, (size_t)(recv_cnt[peer] * rec), ncclUint8, peer, c->nccl, s));
+      if (srec > 0 && send_scnt[peer] > 0)
+        UB_CHECK_NCCL(ncclSend(w.send_smp + sso * srec, (size_t)(send_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
+      if (srec > 0 && recv_scnt[peer] > 0)
+        UB_CHECK_NCCL(ncclRecv(w.recv_smp + rso * srec, (size_t)(recv_scnt[peer] * srec), ncclUint8, peer, c->nccl, s));
+      c->nccl_ops += (send_cnt[peer] > 0) + (recv_cnt[peer] > 0) + (srec > 0 && send_scnt[peer] > 0) +
+                     (srec > 0 && recv_scnt[peer] > 0);
       so += send_cnt[peer]; ro += recv_cnt[peer]; sso += send_scnt[peer]; rso += recv_scnt[peer];
     }
     UB_CHECK_NCCL(ncclGroupEnd());
   }
   UB_PHASE();
-  // 6. reorder the per-source chunks into perm order (a5)
-  if ((st = ub_exchange_copy(w.recv_tok, d_out_tokens, w.recv_smp, d_out_samples, w.tab_unpack, B, rec, srec, s)) !=
-      UB_OK)
+  // 6. reorder into perm order (a5): kept samples from this rank's own buffer, the others from
+  // the receive buffer; the same launch writes the new cu_seqlens (the input-only
+  // operators run during the exchange)
+  if ((st = exchange_gather(d_my_tokens, w.recv_tok, d_out_tokens, d_my_samples, w.recv_smp, d_out_samples,
+                            w.stage + (size_t)5 * B, w.stage + (size_t)10 * B, B, B, rec, srec,
+                            reinterpret_cast<const int32_t*>(w.stage + (size_t)11 * B), d_out_cu, B + 1, s)) != UB_OK)
     return st;
-  // 7. the new cu_seqlens, computed on the host (input-only operators run during the exchange)
-  c->h_cu[0] = 0;
-  for (int32_t k = 0; k < B; ++k) c->h_cu[k + 1] = c->h_cu[k] + h_all[perm[(size_t)me * B + k]];
-  UB_CHECK_CUDA(cudaMemcpyAsync(d_out_cu, c->h_cu, sizeof(int32_t) * (B + 1), cudaMemcpyHostToDevice, s));
   UB_CHECK_CUDA(cudaEventRecord(c->ev_staging, s));
   UB_PHASE();
 #undef UB_PHASE

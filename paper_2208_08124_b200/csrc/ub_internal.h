@@ -94,6 +94,13 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// exchange copy (unpad_pad.cu): n entries of a {src_tok, len, dst_tok, src_smp, dst_smp} table with
+// row stride B; d_sel (row of n, may be NULL) picks src_b / ssrc_b for entries != 0; cu_dst (may be
+// NULL) receives ncu int32 from cu_src in the same launch.
+ub_status exchange_gather(const void* src_a, const void* src_b, void* dst, const void* ssrc_a, const void* ssrc_b,
+                          void* sdst, const int64_t* d_tab, const int64_t* d_sel, int32_t n, int32_t B, int64_t rec,
+                          int64_t srec, const int32_t* cu_src, int32_t* cu_dst, int32_t ncu, cudaStream_t s);
+
 // checked mode (checked.cu): validate device cu_seqlens before a launch (sync; tests only)
 bool checked_mode();
 ub_status checked_cu(const int32_t* d_cu, int32_t B, int32_t max_seqlen, int64_t T, cudaStream_t s);

@@ -196,24 +196,61 @@ static ub_status unpad_pad_dispatch(bool pad, const void* src, void* dst, const 
 
 // ------------------------------------------------------------------ exchange copy
 // One CTA (or gridDim.y CTAs) per table entry: copies len*rec bytes of token records and srec bytes of the
-// sample record.  tab = {src_tok[B], len[B], dst_tok[B], src_smp[B], dst_smp[B]}.
+// sample record.  tab = {src_tok[B], len[B], dst_tok[B], src_smp[B], dst_smp[B]} (row stride B, gridDim.x
+// entries).  Gather form (the exchange's final reorder): a sixth row sel[B] picks the source per entry
+// (0: st / ss, 1: st_b / ss_b -- this rank's own packed samples vs the receive buffer), and CTA (0, 0)
+// also copies ncu int32 from cu_src to cu_dst (the new cu_seqlens staged with the tables).
 template <typename Vec>
-__global__ void __launch_bounds__(256) exchange_copy_kernel(const uint8_t* __restrict__ st, uint8_t* __restrict__ dt,
-                                                            const uint8_t* __restrict__ ss, uint8_t* __restrict__ ds,
-                                                            const int64_t* __restrict__ tab, int32_t B,
-                                                            int64_t rec, int64_t srec) {
+__global__ void __launch_bounds__(256) exchange_copy_kernel(const uint8_t* __restrict__ st, const uint8_t* __restrict__ st_b,
+                                                            uint8_t* __restrict__ dt, const uint8_t* __restrict__ ss,
+                                                            const uint8_t* __restrict__ ss_b, uint8_t* __restrict__ ds,
+                                                            const int64_t* __restrict__ tab, const int64_t* __restrict__ sel,
+                                                            int32_t B, int64_t rec, int64_t srec,
+                                                            const int32_t* __restrict__ cu_src, int32_t* __restrict__ cu_dst,
+                                                            int32_t ncu) {
   const int e = blockIdx.x;
+  if (cu_dst != nullptr && e == 0 && blockIdx.y == 0)
+    for (int32_t i = threadIdx.x; i < ncu; i += blockDim.x) cu_dst[i] = cu_src[i];
   const int64_t src_tok = tab[e], len = tab[B + e], dst_tok = tab[2 * B + e];
-  const Vec* s = reinterpret_cast<const Vec*>(st + src_tok * rec);
+  const bool alt = sel != nullptr && sel[e] != 0;
+  const Vec* s = reinterpret_cast<const Vec*>((alt ? st_b : st) + src_tok * rec);
   Vec* d = reinterpret_cast<Vec*>(dt + dst_tok * rec);
   const int64_t nv = len * rec / (int64_t)sizeof(Vec);
   // gridDim.y CTAs share an entry (large records): interleaved 256-vector blocks
   for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.y * blockDim.x)
     d[i] = s[i];
   if (srec > 0 && blockIdx.y == 0) {
+    const uint8_t* sp = alt ? ss_b : ss;
     const int64_t so = tab[3 * B + e] * srec, dso = tab[4 * B + e] * srec;
-    for (int64_t i = threadIdx.x; i < srec; i += blockDim.x) ds[dso + i] = ss[so + i];
+    for (int64_t i = threadIdx.x; i < srec; i += blockDim.x) ds[dso + i] = sp[so + i];
   }
+}
+
+ub_status exchange_gather(const void* src_a, const void* src_b, void* dst, const void* ssrc_a, const void* ssrc_b,
+                          void* sdst, const int64_t* d_tab, const int64_t* d_sel, int32_t n, int32_t B, int64_t rec,
+                          int64_t srec, const int32_t* cu_src, int32_t* cu_dst, int32_t ncu, cudaStream_t s) {
+  if (n <= 0 && cu_dst == nullptr) return UB_OK;
+  const uintptr_t al = (uintptr_t)src_a | (uintptr_t)(src_b ? src_b : src_a) | (uintptr_t)dst;
+  auto* sa = static_cast<const uint8_t*>(src_a);
+  auto* sb = static_cast<const uint8_t*>(src_b);
+  auto* dt = static_cast<uint8_t*>(dst);
+  auto* ssa = static_cast<const uint8_t*>(ssrc_a);
+  auto* ssb = static_cast<const uint8_t*>(ssrc_b);
+  auto* ds = static_cast<uint8_t*>(sdst);
+  const dim3 grid(n > 0 ? n : 1, rec >= 256 ? 16 : 1);     // large records: 16 CTAs per entry
+  if (n <= 0) {                                           // nothing to move: only the cu copy
+    exchange_copy_kernel<uint8_t><<<1, 256, 0, s>>>(sa, sb, dt, ssa, ssb, ds, d_tab, nullptr, B, 0, 0, cu_src, cu_dst, ncu);
+  } else if (rec % 16 == 0 && (al & 15) == 0) {
+    exchange_copy_kernel<int4><<<grid, 256, 0, s>>>(sa, sb, dt, ssa, ssb, ds, d_tab, d_sel, B, rec, srec, cu_src, cu_dst, ncu);
+  } else if (rec % 4 == 0 && (al & 3) == 0) {
+    exchange_copy_kernel<uint32_t><<<grid, 256, 0, s>>>(sa, sb, dt, ssa, ssb, ds, d_tab, d_sel, B, rec, srec, cu_src, cu_dst,
+                                                        ncu);
+  } else {
+    exchange_copy_kernel<uint8_t><<<grid, 256, 0, s>>>(sa, sb, dt, ssa, ssb, ds, d_tab, d_sel, B, rec, srec, cu_src, cu_dst,
+                                                       ncu);
+  }
+  UB_CHECK_LAUNCH();
+  return UB_OK;
 }
 
 }  // namespace ub
@@ -237,19 +274,10 @@ extern "C" ub_status ub_exchange_copy(const void* src_tokens, void* dst_tokens, 
   UB_REQUIRE(src_tokens && dst_tokens && d_tab, UB_ERR_INVALID_ARG, "null pointer");
   UB_REQUIRE(B >= 1 && rec_bytes > 0 && srec_bytes >= 0, UB_ERR_SHAPE, "bad sizes");
   UB_REQUIRE(srec_bytes == 0 || (src_samples && dst_samples), UB_ERR_INVALID_ARG, "null sample pointer");
-  cudaStream_t s = as_stream(stream);
-  const uintptr_t al = (uintptr_t)src_tokens | (uintptr_t)dst_tokens;
-  auto* st = static_cast<const uint8_t*>(src_tokens);
-  auto* dt = static_cast<uint8_t*>(dst_tokens);
-  auto* ss = static_cast<const uint8_t*>(src_samples);
-  auto* ds = static_cast<uint8_t*>(dst_samples);
-  const dim3 grid(B, rec_bytes >= 256 ? 16 : 1);     // large records: 16 CTAs per entry
-  if (rec_bytes % 16 == 0 && (al & 15) == 0)
-    exchange_copy_kernel<int4><<<grid, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
-  else if (rec_bytes % 4 == 0 && (al & 3) == 0)
-    exchange_copy_kernel<uint32_t><<<grid, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
-  else
-    exchange_copy_kernel<uint8_t><<<grid, 256, 0, s>>>(st, dt, ss, ds, d_tab, B, rec_bytes, srec_bytes);
+  if (ub_status st = exchange_gather(src_tokens, nullptr, dst_tokens, src_samples, nullptr, dst_samples, d_tab, nullptr, B, B,
+                                     rec_bytes, srec_bytes, nullptr, nullptr, 0, as_stream(stream));
+      st != UB_OK)
+    return st;
   UB_CHECK_LAUNCH();
   return UB_OK;
 }

@@ -1,7 +1,7 @@
-"""Correlate the warps of CTA 0 in a bwd trace build, per pair p (cycles from kernel start):
-producer stage wait passed (23) / arrived (24); MMA: P_p seen + dV_p issue (12), S_{p+1}
-issued (10), dK_p/dQ_p/dP_{p+1} issued (19); compute warp 0: waiting (1), S_p in (2), exp done
-(3), P_p stored (4), dP_p in (5), dS_p stored (7); epilogue warp 8: dQ_p in (31), out (32)."""
+"""Correlate the warps of CTA 0 in a bwd trace build, per iteration / pair j (cycles from kernel
+start): producer stage wait passed (23) / arrived (24); MMA: S_{j+1}, dP_j issued (10), P~_j seen
+(12), dS_{j-1} seen (13), dK/dQ issued (19); compute warp 0: iteration start (1), S_j / dP_{j-1}
+waits passed (2), P~_j stored (4), dS_{j-1} stored (7); epilogue warp 8: dQ in (31), out (32)."""
 import ctypes as C, sys
 sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
 import numpy as np, torch
@@ -22,10 +22,10 @@ ev = (buf >> np.uint64(48)).astype(np.int64); ck = (buf & np.uint64(0xFFFFFFFFFF
 t0 = ck[ck > 0].min()
 def series(w, e):
     return [int(ck[w * 1024 + i] - t0) for i in range(1024) if buf[w * 1024 + i] and ev[w * 1024 + i] == e]
-cols = [("pSt", 12, 23), ("pArr", 12, 24), ("mP+dV", 13, 12), ("mS+1", 13, 10), ("mGr", 13, 19),
-        ("c1", 0, 1), ("cS", 0, 2), ("cExp", 0, 3), ("cP", 0, 4), ("cdP", 0, 5), ("cdS", 0, 7),
-        ("eQin", 8, 31), ("eQout", 8, 32)]
+cols = [("pSt", 12, 23), ("pArr", 12, 24), ("mSdP", 13, 10), ("mdV", 13, 12), ("mdKQ", 13, 13), ("mGrd", 13, 19),
+        ("c1", 0, 1), ("cIn", 0, 2), ("cP", 0, 4), ("cdS", 0, 7),
+        ("eQin", 8, 31), ("eKV", 8, 33), ("eQfree", 8, 34), ("eQout", 8, 32)]
 ser = {n: series(w, e) for n, w, e in cols}
 print("pair " + " ".join(f"{n:>7s}" for n, _, _ in cols))
-for p in range(min(40, len(ser["cS"]))):
+for p in range(min(40, len(ser["cIn"]))):
     print(f"{p:4d} " + " ".join(f"{(ser[n][p] if p < len(ser[n]) else -1):7d}" for n, _, _ in cols))
