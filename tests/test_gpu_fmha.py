@@ -58,6 +58,19 @@ def test_bf16_edge_lengths_fwd_bwd(ub, p):
         assert_close(d[:, i].float().numpy(), dq[:, i], "d" + name)
 
 
+def test_bf16_longer_than_in_kernel_delta(ub):
+    """max_seqlen > 512: the backward takes its Delta from the separate row-dot kernel instead
+    of computing it per item in shared memory; both paths against the oracle (L = 700, 129)."""
+    lengths, off, qkv, dout, o, lse, d, scale = _run(ub, [700, 129, 5], 2, 64, torch.bfloat16, p=0.1,
+                                                     max_seqlen=768)
+    q64, g64 = qkv.double().numpy(), dout.double().numpy()
+    O, LSE = oatt.varlen_fwd(q64, off, 768, scale, 0.1, 7, 0)
+    assert_close(o.float().numpy(), O, "O")
+    dq = oatt.varlen_bwd(q64, g64, off, 768, scale, 0.1, 7, 0)
+    for i, name in enumerate("qkv"):
+        assert_close(d[:, i].float().numpy(), dq[:, i], "d" + name)
+
+
 def test_bf16_fwd_deterministic_and_single_sequence(ub):
     lengths, off, qkv, dout = make_batch([200, 77], 3, 64)
     cu = torch.tensor(off.astype(np.int32)).cuda()
