@@ -693,6 +693,23 @@ def gather_bench(wl, peaks, iters=20):
         gbs = nbytes / (us * 1e-6) / 1e9
         out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
                      "bytes": int(nbytes)}
+    # the size-matched ceiling: torch's own device copy of the packed tensor (same bytes as unpad;
+    # at ~30 MB the launch ramp and drain keep any copy below the 2-GiB copy that measured the peak)
+    cp = [torch.empty((T, H * D), dtype=torch.bfloat16, device=wl.dev) for _ in range(3)]
+    for k in range(3):
+        cp[k].copy_(bufs[k][1])
+    torch.cuda.synchronize()
+    torch.cuda._sleep(2_000_000)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(iters):
+        cp[k % 3].copy_(bufs[k % 3][1])
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / iters * 1e3
+    out["torch_copy_same_bytes"] = {"us": round(us, 2), "GBps": round(2 * T * row / (us * 1e-6) / 1e9, 1),
+                                    "frac_hbm": round(2 * T * row / (us * 1e-6) / 1e9 / peaks["hbm"], 3),
+                                    "note": "torch copy_ of the packed tensor: the achievable copy rate at this size"}
     out["shape"] = f"hidden [{B}, {S}, {H * D}] bf16 <-> [T={T}, {H * D}]"
     # NEXT-3: the exchange's data movement at SURVEY §8(a) a4's stress record size (a bf16
     # hidden row, 2 kB per token), one rank: the pull gather (one pass) against the NCCL

@@ -64,9 +64,21 @@ __global__ void __launch_bounds__(256) unpad_pad_kernel(const Vec* __restrict__ 
 // copies, and pad's zero fill is B contiguous runs whose prefix offsets are the same delta_b.
 // Each CTA takes a fixed span of the packed (or zero) vector space, finds its first
 // sequence by one binary search, and streams 16-B vectors with several loads in flight.
-constexpr int kSpanThreads = 256;
-constexpr int kSpanUnroll = 4;
-constexpr int64_t kSpanVecs = (int64_t)kSpanThreads * kSpanUnroll * 4;   // 64 KB per CTA
+#ifndef UB_SPAN_UNROLL
+#define UB_SPAN_UNROLL 4
+#endif
+#ifndef UB_SPAN_ITERS
+#define UB_SPAN_ITERS 1
+#endif
+#ifndef UB_SPAN_THREADS
+#define UB_SPAN_THREADS 256
+#endif
+constexpr int kSpanThreads = UB_SPAN_THREADS;
+constexpr int kSpanUnroll = UB_SPAN_UNROLL;           // 16-B loads in flight per thread
+// 16 KB per CTA: measured on the config-2 hidden state (B200, 3 rotating buffer sets) against
+// 64 KB per CTA: unpad 13.8 -> 12.1 us (0.75 of HBM; torch's own copy of the packed tensor:
+// 12.4 us), pad 17.6 -> 16.1 us (0.84); 8 loads in flight or 512 threads per CTA were slower
+constexpr int64_t kSpanVecs = (int64_t)kSpanThreads * kSpanUnroll * UB_SPAN_ITERS;   // 16-B vectors per CTA
 
 __device__ __forceinline__ int32_t seq_of(const int32_t* __restrict__ cu, int32_t B, int64_t key, int64_t V, int32_t S,
                                           bool zero_space) {

@@ -21,7 +21,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
         "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "sm__cycles_elapsed.avg", "gpc__cycles_elapsed.avg.per_second"]
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+        "ns": 1e-9, "us": 1e-6, "ms": 1e-3}
 
 
 def raw(rep):
@@ -55,6 +56,31 @@ def main(tag):
         summ["dram_bytes_per_launch"]["fmha_" + k] = rb + wb
         with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_{k}_raw.csv"), "w") as f:
             csv.writer(f).writerows(rows)
+    # HBM-bound gather kernels (a5 / a6 / a9): one metrics row per launch
+    gp = os.path.join(ROOT, "gpurun_out", f"gather_{tag}.csv")
+    if os.path.exists(gp):
+        lines = [l for l in open(gp) if not l.startswith("==")]
+        rows = list(csv.reader(io.StringIO("".join(lines))))
+        hdr = rows[0]
+        ki, mi, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+        per = {}
+        idi = hdr.index("ID")
+        for r in rows[1:]:
+            if len(r) <= vi:
+                continue
+            v = float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1)
+            per.setdefault((r[idi], r[ki][:60]), {})[r[mi]] = v
+        out = []
+        for (lid, k), m in per.items():
+            t = m.get("gpu__time_duration.sum", 0.0)
+            by = m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+            out.append({"kernel": k, "us": round(t * 1e6, 2), "dram_bytes": by,
+                        "dram_GBps": round(by / t / 1e9, 1) if t else None})
+        with open(os.path.join(ROOT, "profiles", f"{tag}_gather_ncu.json"), "w") as f:
+            json.dump(out, f, indent=1)
+        rnd["gather"] = f"profiles/{tag}_gather_ncu.json"
+        for e in out:
+            summ["dram_bytes_per_launch"].setdefault("gather", {})[e["kernel"]] = e["dram_bytes"]
     lp = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     if os.path.exists(lp):
         lines = [l for l in open(lp) if not l.startswith("==")]
