@@ -56,7 +56,8 @@ SREC = 4      # per-sample record: next_sentence_label (int32)
 N_SETS = 3    # rotating input sets: each step's working set (> 300 MB) and the 2 others exceed L2
 N_EX = 5      # exchange output buffers in flight: the side stream never waits on the step just enqueued
 PIPE = 3      # step n computes while step n+PIPE is exchanged and n+PIPE+1's lengths are gathered
-KERNELS_PER_STEP = 6    # ours: unpad, 2x exchange copy, fwd main (+ fused pad), bwd pre (Delta) + main
+KERNELS_PER_STEP = 5    # ours at W = 1: unpad, exchange gather, fwd main (+ fused pad), bwd pre (Delta) + main,
+                        # plus the dropout-mask kernel when p > 0
 
 
 def parse():
@@ -66,16 +67,20 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--dist", default="mlperf_like_v0", choices=list(synth.DISTRIBUTIONS))
-    ap.add_argument("--p-dropout", type=float, default=0.0)
+    ap.add_argument("--p-dropout", type=float, default=0.1,
+                    help="attention dropout of the headline step: 0.1, BERT-large's value, as SURVEY §8(d) "
+                         "names the headline; the same step at p = 0 is reported beside it (p0_step)")
     ap.add_argument("--balance", default="paper",
                     choices=["paper", "snake", "lpt", "stay", "paper+locality", "snake+locality", "lpt+locality"])
     ap.add_argument("--skew", default="iid", choices=["iid", "sorted-block"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-encoder", action="store_true", help="skip the NEXT-1 encoder sub-layer measurement")
-    ap.add_argument("--prof-every", type=int, default=4,
-                    help="record the per-kernel events on every k-th timed step (event records between kernels "
-                         "block their programmatic-dependent-launch overlap)")
+    ap.add_argument("--prof-every", type=int, default=0,
+                    help="record the per-kernel events on every k-th step of the headline region; 0 (default): "
+                         "the headline region runs uninstrumented (event records between kernels block their "
+                         "programmatic-dependent-launch overlap, ~13 us per step) and the per-kernel times come "
+                         "from a separate instrumented region of the same steps")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--reserve-sms", type=int, default=4,
                     help="SMs the persistent FMHA grid leaves to the side-stream exchange (r02c: 0 left the "
@@ -366,6 +371,10 @@ class Workload:
         self.lse = torch.empty((H, self.cap), dtype=torch.float32, device=dev)
         self.lse_buf = self.lse                               # the hot loop's [H, T] view of the same memory
         self._begin, self._finish, self._unpad, self._fmha, self._prof_on = {}, {}, {}, {}, False
+        self._mask = {}
+        self.p = args.p_dropout
+        # R5's keep bits, materialised once per step (ub_dropout_mask) and read by both directions
+        self.mask_buf = torch.empty(ub.api.dropout_mask_bytes(self.cap, H, S), dtype=torch.uint8, device=dev)
         self.dqkv = torch.empty((self.cap, 3, H, D), dtype=torch.bfloat16, device=dev)
         self.padded_out = torch.empty((B, S, H, D), dtype=torch.bfloat16, device=dev)
         # the compute stream at the highest priority, the exchange at the lowest: when an SM
@@ -438,14 +447,25 @@ class Workload:
     def bound(self, n):
         """The pre-marshalled FMHA calls of step n's buffers (input set, exchange slot, dqkv)."""
         s, e = n % N_SETS, n % N_EX
-        key = (s, e, self.dqkv.data_ptr())
+        key = (s, e, self.dqkv.data_ptr(), self.p)
         b = self._fmha.get(key)
         if b is None:
             st = self.sets[s]
             b = self._fmha[key] = self.ub.api.BoundFmha(
                 st["qkv"], self.ex[e]["cu"], S, self.out, self.lse_buf, dout=st["dout"], dqkv=self.dqkv,
-                p_dropout=self.args.p_dropout, stream=self.main, num_ctas=self.ctas, padded=self.padded_out)
+                p_dropout=self.p, stream=self.main, num_ctas=self.ctas, padded=self.padded_out,
+                dropout_mask=self.mask_buf if self.p > 0 else None)
         return b
+
+    def mask(self, n):
+        """ub_dropout_mask of step n's exchanged batch (cu_seqlens of its exchange slot)."""
+        e = n % N_EX
+        key = (e, self.p)
+        m = self._mask.get(key)
+        if m is None:
+            m = self._mask[key] = self.ub.api.BoundDropoutMask(self.ex[e]["cu"], self.cap, H, S, self.p,
+                                                               self.mask_buf, stream=self.main)
+        return m
 
     def step(self, n, prof=None, marks=None):
         """Main stream: a7 fwd (+ fused a9 pad), a8 bwd for step n.  marks: host timestamps."""
@@ -463,6 +483,8 @@ class Workload:
         if marks is not None:
             marks.append(time.perf_counter())
         b = self.bound(n)
+        if self.p > 0:
+            self.mask(n)(T, 0x2208 + n)                     # keep bits for both directions of this step
         # a7 + a9: the forward's epilogue also writes the padded copy of O, zeros past
         # each length -- the separate pad pass is gone (ub_varlen_fmha_fwd_pad)
         b.fwd(T, 0x2208 + n)
@@ -517,7 +539,7 @@ def run_ours(args, world, rank, local):
         step_ev[k].record(wl.main)
         h0 = time.perf_counter()
         m = []
-        profiled = k % args.prof_every == 0
+        profiled = args.prof_every > 0 and k % args.prof_every == 0
         tokens += wl.step(n, prof_events[k] if profiled else None, m)
         lens_used.append((n, wl.ex[n % N_EX]["perm"]))      # a reference; lengths derived after the loop
         h1 = time.perf_counter()
@@ -549,9 +571,20 @@ def run_ours(args, world, rank, local):
     per_rank_tokens = all_gather_list(tokens / args.steps, world)
     imbalance = max(per_rank_tokens) / (sum(per_rank_tokens) / world) - 1.0
 
-    # per-kernel device time (events on the launching stream)
-    prof_steps = [i for i in range(args.steps) if i % args.prof_every == 0]
-    kt = {k: [prof_events[i][k][0].elapsed_time(prof_events[i][k][1]) for i in prof_steps] for k in kids}
+    # per-kernel device time (events the library records around its own launches, on the
+    # launching stream): from the headline region (--prof-every k) or, by default, from a
+    # separate region of the same pipelined steps with every step instrumented
+    if args.prof_every > 0:
+        prof_steps = [i for i in range(args.steps) if i % args.prof_every == 0]
+        kt = {k: [prof_events[i][k][0].elapsed_time(prof_events[i][k][1]) for i in prof_steps] for k in kids}
+        instr_ms = None
+    else:
+        rec = []
+        instr_ms, _, _ = pipelined_region(wl, args, world, last + 1 + 20 * N_EX, args.p_dropout, prof=rec)
+        prof_steps = list(range(len(rec)))
+        kt = {k: [rec[i][2][k][0].elapsed_time(rec[i][2][k][1]) for i in prof_steps] for k in kids}
+        lens_used = [np.asarray(wl.all_lengths_cache(nn), np.int64)[pp[rank * B:(rank + 1) * B]] for nn, pp, _ in rec]
+        prof_events = [r[2] for r in rec]
     f_fwd = [flops_fwd(lens_used[i]) for i in prof_steps]
     f_bwd = [flops_bwd(lens_used[i]) for i in prof_steps]
     fwd_us, bwd_us = np.mean(kt[kids[0]]) * 1e3, np.mean(kt[kids[1]]) * 1e3
@@ -583,25 +616,39 @@ def run_ours(args, world, rank, local):
     P = prof_events
     F, Bk = kids[0], kids[1]
     f2b = float(np.mean([P[i][F][1].elapsed_time(P[i][Bk][0]) for i in prof_steps])) * 1e3
+    step_ref = (instr_ms * 1e3) if instr_ms is not None else ms_max / args.steps * 1e3
     timeline = {"fwd_end_to_bwd_main_us": round(f2b, 2),
-                "rest_of_step_us": round(ms_max / args.steps * 1e3 - fwd_us - bwd_us - f2b, 2),
-                "kernel_events_on": f"every {args.prof_every} step(s); the others run uninstrumented"}
+                "rest_of_step_us": round(step_ref - fwd_us - bwd_us - f2b, 2),
+                "kernel_events_on": (f"every {args.prof_every} step(s) of the headline region" if args.prof_every
+                                     else f"every step of a separate instrumented region "
+                                          f"({round(step_ref, 2)} us per step there)")}
 
+    # the same pipelined step without attention dropout (p = 0), beside the headline
+    p0 = None
+    if args.p_dropout > 0:
+        ms0, tok0, _ = pipelined_region(wl, args, world, last + 1 + 10 * N_EX, 0.0)
+        p0 = {"value": round(tok0 / (ms0 / 1e3), 1), "unit": "tokens/s", "ms_per_step": round(ms0, 4),
+              "p_dropout": 0.0, "note": "the headline's pipelined step (exchange overlapped) at p = 0"}
+        wl.p = args.p_dropout
     e2e = None if args.no_e2e else run_e2e(args, wl, world)
     gather = gather_bench(wl, peaks) if rank == 0 else None
     encoder = encoder_bench(wl, peaks) if rank == 0 and not args.no_encoder else None
     embedding = embedding_bench(wl, peaks) if rank == 0 and not args.no_encoder else None
-    drop01 = dropout_bench(wl) if rank == 0 and args.p_dropout == 0.0 else None
+    drop01 = dropout_bench(wl) if rank == 0 else None
     sweep = dist_sweep(wl, peaks) if rank == 0 and not args.no_encoder else None
     out = {"metric": "unpadded FMHA fwd+bwd tokens/s (BERT-large)", "value": round(value, 1), "unit": "tokens/s",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
            "data": "synthetic (seeded lengths + N(0,1) bf16 qkv/dO; no dataset)",
            "config": {"workload": f"bert_large_fmha_{args.dist}", "batch_per_gpu": B, "heads": H, "head_dim": D,
-                      "max_seqlen": S, "p_dropout": args.p_dropout, "balance": args.balance, "skew": args.skew,
+                      "max_seqlen": S, "p_dropout": args.p_dropout,
+                      "p_dropout_applied": ub.api.dropout_effective_p(args.p_dropout) if args.p_dropout > 0 else 0.0,
+                      "balance": args.balance, "skew": args.skew,
                       "parallelism": f"dp{world}", "fmha_ctas": wl.ctas, "exchange": args.exchange, "l2": "rotating 3 input sets; per-step working set > L2",
-                      "step": "unpad records + exchange (side stream) | fmha fwd with fused pad + bwd (main stream)"},
+                      "step": "unpad records + exchange (side stream) | dropout keep bits (p > 0), fmha fwd with fused "
+                   "pad, bwd (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),
+           "p0_step": p0,
            "tc_util": tc_util,
            "imbalance": round(imbalance, 5), "planned_imbalance": planned_imbalance(args),
            "step_us_distribution": {"p10": round(float(np.percentile(step_us, 10)), 2),
@@ -612,7 +659,7 @@ def run_ours(args, world, rank, local):
                                             "K-step region / K"},
            "exchange_overlap": overlap,
            "main_stream_timeline": timeline, "attn_dropout_0.1": drop01, "length_sweep": sweep, "gather": gather,
-           "encoder_attn_sublayer": encoder, "embedding": embedding, "gpu_launches": KERNELS_PER_STEP * args.steps, "clocks": clk,
+           "encoder_attn_sublayer": encoder, "embedding": embedding, "gpu_launches": (KERNELS_PER_STEP + (1 if args.p_dropout > 0 else 0)) * args.steps, "clocks": clk,
            "host_us_per_step": dict(zip(["step_setup", "fwd_call", "bwd_call", "pad_call", "unpad_call", "finish_call",
                                               "begin_call"],
                                         [round(1e6 * float(x), 1) for x in np.median(np.array(marks), axis=0)]),
@@ -621,6 +668,58 @@ def run_ours(args, world, rank, local):
     if e2e is not None:
         out["e2e"] = e2e
     return out, wl
+
+
+def pipelined_region(wl, args, world, first, p, prof=None):
+    """The headline's step loop (exchange pipelined on the side stream) at dropout p, started
+    at step number `first` on an empty pipeline: returns (ms per step, max over ranks; tokens
+    per step summed over ranks; next free step number).  prof: a list that receives, per
+    timed step, (step number, perm reference, {kernel id: (start, stop) events}) with the
+    library's per-kernel events recorded on every step."""
+    wl.p = p
+    for n in range(first, first + PIPE + 1):
+        wl.begin(n)
+    for n in range(first, first + PIPE):
+        wl.finish(n)
+    n = first
+    for _ in range(args.warmup):
+        wl.step(n)
+        wl.finish(n + PIPE)
+        wl.begin(n + PIPE + 1)
+        n += 1
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(wl.main)
+    tok = 0
+    kids = (0, 1, 3)
+    evs = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in kids}
+           for _ in range(args.steps)] if prof is not None else None
+    if evs:
+        for d in evs:
+            for a, b_ in d.values():
+                a.record(wl.main)
+                b_.record(wl.main)
+        e0.record(wl.main)
+    for k in range(args.steps):
+        tok += wl.step(n, evs[k] if evs else None)
+        if prof is not None:
+            prof.append((n, wl.ex[n % N_EX]["perm"], evs[k]))
+        wl.finish(n + PIPE)
+        wl.begin(n + PIPE + 1)
+        n += 1
+    wl.main.wait_stream(wl.side)
+    e1.record(wl.main)
+    if evs:
+        for kid in kids:
+            wl.ub.api.profile_events(kid)
+        wl._prof_on = False
+    torch.cuda.synchronize()
+    barrier(world)
+    wl.finish(n + PIPE)
+    torch.cuda.synchronize()
+    ms = all_max(e0.elapsed_time(e1), world) / args.steps
+    return ms, all_sum(tok, world) / args.steps, n + PIPE + 1
 
 
 def exchange_overlap(args, wl, world, last, step_us):
@@ -771,30 +870,48 @@ def gather_bench(wl, peaks, iters=20):
 
 
 def dropout_bench(wl, iters=10):
-    """The same FMHA fwd + bwd at attention dropout p = 0.1 (BERT-large's training value,
-    SURVEY §8(d)), device time of the main kernels from the library's events."""
+    """Attention dropout p = 0.1 (BERT-large's training value) two ways on one
+    batch: keep bits regenerated by Philox inside the FMHA kernels (no mask argument), and
+    materialised once by ub_dropout_mask and read by both kernels (the headline step's way).
+    Device time of each kernel from the library's events / CUDA events."""
     from paper_2208_08124_b200 import api
     ub = wl.ub
     st, ex = wl.sets[0], wl.ex[0]
     T = ex["T"]
     qkv, dout = st["qkv"][:T], st["dout"][:T]
     cu = ex["cu"]
+    m = api.dropout_mask(cu, T, H, S, 0.1, 7, 0)
     o, lse = ub.varlen_fmha_fwd(qkv, cu, S, None, 0.1, 7, 0)
     res = {}
-    for name, kid, fn in (("fwd", api.PROF_FWD, lambda: ub.varlen_fmha_fwd(qkv, cu, S, None, 0.1, 7, 0, out=o, lse=lse)),
-                          ("bwd", api.PROF_BWD, lambda: ub.varlen_fmha_bwd(qkv, o, lse, dout, cu, S, None, 0.1, 7, 0))):
+
+    def timed(kid, fn):
         fn()
         torch.cuda.synchronize()
         torch.cuda._sleep(2_000_000)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
         for k in range(iters):
-            api.profile_events(kid, *ev[k])
-            fn()
-        api.profile_events(kid)
+            if kid is None:
+                ev[k][0].record()
+                fn()
+                ev[k][1].record()
+            else:
+                api.profile_events(kid, *ev[k])
+                fn()
+        if kid is not None:
+            api.profile_events(kid)
         torch.cuda.synchronize()
-        res[name + "_us"] = round(float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3, 2)
-    res["fmha_only_tokens_per_s"] = round(T / ((res["fwd_us"] + res["bwd_us"]) * 1e-6), 1)
-    res["note"] = "main kernels only, L2-warm single batch; headline runs p = 0 (config 2 names no dropout)"
+        return round(float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3, 2)
+    for tag, mk in (("philox_in_kernel", None), ("mask", m)):
+        r = {"fwd_us": timed(api.PROF_FWD, lambda: ub.varlen_fmha_fwd(qkv, cu, S, None, 0.1, 7, 0, out=o, lse=lse,
+                                                                       dropout_mask=mk)),
+             "bwd_us": timed(api.PROF_BWD, lambda: ub.varlen_fmha_bwd(qkv, o, lse, dout, cu, S, None, 0.1, 7, 0,
+                                                                       dropout_mask=mk))}
+        if mk is not None:
+            r["mask_us"] = timed(None, lambda: api.dropout_mask(cu, T, H, S, 0.1, 7, 0, out=m))
+        tot = r["fwd_us"] + r["bwd_us"] + r.get("mask_us", 0.0)
+        r["fmha_only_tokens_per_s"] = round(T / (tot * 1e-6), 1)
+        res[tag] = r
+    res["note"] = "main kernels (and the mask kernel), L2-warm single batch, p = 0.1 (applied 25/256)"
     return res
 
 

@@ -131,9 +131,24 @@ typedef struct {
   int32_t dtype;      /* ub_dtype */
   int32_t num_ctas;   /* persistent grid size; 0 = one CTA per SM.  Set below the SM count to
                          leave SMs to concurrent side-stream work (the overlapped exchange) */
+  const void* dropout_mask; /* p > 0 only: the keep bits ub_dropout_mask wrote for these params and
+                         cu_seqlens (device, ub_dropout_mask_bytes), read by the forward and the
+                         backward; NULL = the kernels regenerate them by Philox as they go (the
+                         same bits: results are bitwise identical either way) */
 } ub_fmha_params;
 
 size_t ub_fmha_workspace_bytes(const ub_fmha_params* prm, int is_bwd);
+
+/* The attention-dropout keep mask of R5 materialised as bits (an input-only operator, P:402:
+ * it needs cu_seqlens, seed and offset only, so it can be produced while the batch is still
+ * being exchanged, once per step for both directions).  Writes two layouts into d_mask
+ * (device, ub_dropout_mask_bytes(prm) bytes, 16-B aligned), MT = ceil(max_seqlen / 128):
+ *   query-major words [H][T][MT][4]: bit e of word w = keep(query row t, key 128 kt + 32 w + e)
+ *   key-major words   [H][T][MT][4]: bit e of word c = keep(query 128 it + 32 c + e, key row t)
+ * (t packed rows, keys / queries counted inside the sequence; words of rows past a sequence
+ * end are left unwritten).  Needs 1/256 <= p < 1 (UB_ERR_INVALID_ARG); bf16 path.  Async. */
+size_t ub_dropout_mask_bytes(const ub_fmha_params* prm);
+ub_status ub_dropout_mask(const ub_fmha_params* prm, const int32_t* d_cu, void* d_mask, void* stream);
 
 /* The attention-dropout rate the FMHA kernels apply for a requested p (R5): floor(256 p) / 256
  * with p taken as float32; 0 for p <= 0.  (The Dropout_Add_LayerNorm kernels use 16-bit

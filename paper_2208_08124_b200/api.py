@@ -117,22 +117,38 @@ def pad(packed: torch.Tensor, cu: torch.Tensor, B: int, S: int, pad_row: torch.T
 
 # ------------------------------------------------------------------ varlen FMHA
 def fmha_params(B, T, max_seqlen, heads, head_dim, dtype, scale=None, p_dropout=0.0, seed=0, offset=0,
-                num_ctas=0):
+                num_ctas=0, dropout_mask=None):
     return FmhaParams(B=int(B), T=int(T), max_seqlen=int(max_seqlen), heads=int(heads), head_dim=int(head_dim),
                       scale=float(scale if scale is not None else 1.0 / math.sqrt(head_dim)),
                       p_dropout=float(p_dropout), seed=int(seed), offset=int(offset),
-                      dtype=UB_BF16 if dtype == torch.bfloat16 else UB_FP32, num_ctas=int(num_ctas))
+                      dtype=UB_BF16 if dtype == torch.bfloat16 else UB_FP32, num_ctas=int(num_ctas),
+                      dropout_mask=(dropout_mask.data_ptr() if dropout_mask is not None else None))
+
+
+def dropout_mask(cu: torch.Tensor, T: int, heads: int, max_seqlen: int, p_dropout: float, seed=0, offset=0,
+                 out=None, stream=None):
+    """R5's keep bits for a batch (ub_dropout_mask): a uint8 CUDA tensor to pass to the forward
+    and the backward (dropout_mask=...), so neither regenerates it.  Query-major words first,
+    then key-major (see include/ub.h)."""
+    B = cu.numel() - 1
+    prm = fmha_params(B, T, max_seqlen, heads, 64, torch.bfloat16, None, p_dropout, seed, offset)
+    n = lib().ub_dropout_mask_bytes(C.byref(prm))
+    if out is None:
+        out = torch.empty(n, dtype=torch.uint8, device=cu.device)
+    assert out.numel() >= n
+    check(lib().ub_dropout_mask(C.byref(prm), _ptr(cu), _ptr(out), _stream(stream)))
+    return out
 
 
 def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=None, p_dropout=0.0, seed=0,
-                    offset=0, out=None, lse=None, stream=None, num_ctas=0, padded=None):
+                    offset=0, out=None, lse=None, stream=None, num_ctas=0, padded=None, dropout_mask=None):
     """Eq. (1) over packed qkv [T, 3, H, D]; returns (out [T,H,D], lse [H,T] fp32).
     padded: optional [B, S, H, D] tensor that the forward also fills with O in the padded
     layout, zeros past each length (a9 fused into the epilogue, ub_varlen_fmha_fwd_pad)."""
     T, three, H, D = qkv.shape
     assert three == 3
     B = cu.numel() - 1
-    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas)
+    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas, dropout_mask)
     if out is None:
         out = torch.empty((T, H, D), dtype=qkv.dtype, device=qkv.device)
     if lse is None:
@@ -148,11 +164,11 @@ def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=
 
 
 def varlen_fmha_bwd(qkv, out, lse, dout, cu, max_seqlen: int, scale=None, p_dropout=0.0, seed=0, offset=0,
-                    dqkv=None, stream=None, num_ctas=0):
+                    dqkv=None, stream=None, num_ctas=0, dropout_mask=None):
     """Backward of varlen_fmha_fwd; returns dqkv [T, 3, H, D]."""
     T, _, H, D = qkv.shape
     B = cu.numel() - 1
-    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas)
+    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas, dropout_mask)
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
     ws = _workspace(lib().ub_fmha_workspace_bytes(C.byref(prm), 1), qkv.device, "fmha_bwd")
@@ -171,15 +187,16 @@ class BoundFmha:
     of at least H * T floats, used as a dense [H, T] array."""
 
     def __init__(self, qkv, cu, max_seqlen, out, lse, dout=None, dqkv=None, scale=None, p_dropout=0.0, seed=0,
-                 offset=0, stream=None, num_ctas=0, padded=None):
+                 offset=0, stream=None, num_ctas=0, padded=None, dropout_mask=None):
         cap, three, H, D = qkv.shape
         B = cu.numel() - 1
-        self.prm = fmha_params(B, cap, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas)
+        self.prm = fmha_params(B, cap, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas,
+                               dropout_mask)
         self._p = C.byref(self.prm)
         L = lib()
         ws_f = _workspace(L.ub_fmha_workspace_bytes(self._p, 0), qkv.device, "fmha_fwd")
         ws_b = _workspace(L.ub_fmha_workspace_bytes(self._p, 1), qkv.device, "fmha_bwd")
-        self._keep = (qkv, cu, out, lse, dout, dqkv, padded, ws_f, ws_b)   # keep the buffers alive
+        self._keep = (qkv, cu, out, lse, dout, dqkv, padded, ws_f, ws_b, dropout_mask)   # keep the buffers alive
         st = _stream(stream)
         if padded is not None:
             self._fwd = L.ub_varlen_fmha_fwd_pad
@@ -209,6 +226,33 @@ class BoundFmha:
         st = self._bwd(*self._bwd_args)
         if st:
             check(st)
+
+
+class BoundDropoutMask:
+    """ub_dropout_mask on a fixed output buffer, marshalled once: call with (T, seed).  Size
+    the buffer for the largest T (dropout_mask_bytes(cap, ...))."""
+
+    def __init__(self, cu, cap, heads, max_seqlen, p_dropout, out, offset=0, stream=None):
+        B = cu.numel() - 1
+        self.prm = fmha_params(B, cap, max_seqlen, heads, 64, torch.bfloat16, None, p_dropout, 0, offset)
+        assert out.numel() >= lib().ub_dropout_mask_bytes(C.byref(self.prm))
+        self._keep = (cu, out)
+        self._args = (C.byref(self.prm), _ptr(cu), _ptr(out), _stream(stream))
+        self._f = lib().ub_dropout_mask
+        self.cap = cap
+
+    def __call__(self, T: int, seed: int):
+        assert 0 < T <= self.cap
+        self.prm.T = T
+        self.prm.seed = seed
+        st = self._f(*self._args)
+        if st:
+            check(st)
+
+
+def dropout_mask_bytes(T: int, heads: int, max_seqlen: int) -> int:
+    prm = fmha_params(1, T, max_seqlen, heads, 64, torch.bfloat16, None, 0.1)
+    return int(lib().ub_dropout_mask_bytes(C.byref(prm)))
 
 
 class BoundUnpad:

@@ -1,7 +1,8 @@
 // Varlen FMHA backward on B200 tensor cores (tcgen05 + TMEM + TMA), bf16 in, fp32 accumulate.
 //
-// Chain rule of Eq. (1) per sequence and head; dropout replayed from the Philox
-// key (R4/R5):
+// Chain rule of Eq. (1) per sequence and head; dropout replayed from R5's keep bits,
+// read from the mask ub_dropout_mask materialised (key-major: 8 bytes per thread and pair) or
+// regenerated here by Philox (R4/R5):
 //   Delta_i = sum_d dO_id O_id                                   (prologue kernel)
 //   S^T = K Q^T, P^T = exp(scale S^T - LSE), dP~^T = V dO^T       (recompute, TMEM)
 //   P~ = P M/(1-p), dP = dP~ M/(1-p), dS = P (dP - Delta)          (registers)
@@ -107,6 +108,8 @@ struct Params {
   float scale, scale_log2;
   float rp;
   uint32_t thr, k0, k1, off;
+  const uint2* mk;      // dropout keep bits, key-major [H][T][MT] x 128 queries, as 64-bit halves
+  int32_t MT;
 };
 
 constexpr uint32_t kIdescS = idesc_bf16_f32(128, 128, 0, 0);     // S^T, dP^T: K-major x K-major
@@ -129,7 +132,9 @@ __device__ __forceinline__ uint32_t keep16_cols(uint32_t warp_j0, uint32_t t_q0,
   return bits;
 }
 
-template <bool kDropout, bool kBigB>
+// kDrop: 0 no dropout, 1 keep bits regenerated by Philox in the kernel (lane-cooperative),
+// 2 keep bits read from the materialised mask (ub_dropout_mask, key-major)
+template <int kDrop, bool kBigB>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_constant__ CUtensorMap tmap_do,
                 const __grid_constant__ CUtensorMap tmap_dq, const __grid_constant__ CUtensorMap tmap_dqkv,
@@ -186,6 +191,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   const int32_t G = (int32_t)gridDim.x, cta = (int32_t)blockIdx.x;
 #define UB_ITEMS(r, it) \
   for (int32_t r = 0; next_item<kBigB>(r, sm.items, sm.plan, prm.plan, prm.cu, prm.B, H, 0, cta, G, it); ++r)
+  constexpr bool kDropout = kDrop != 0;
   // each role re-sizes its registers at its entry, inside its branch (ptxas takes the
   // minimum where paths merge); setmaxnreg is warpgroup-uniform
 
@@ -370,10 +376,14 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         const int32_t key = kt * kTile + (int32_t)r;
         const bool key_ok = key < it.L;
         const bool warp_partial = __any_sync(0xffffffffu, !key_ok);     // a sequence's last key tile
-        const uint32_t warp_j0 = (uint32_t)(kt * kTile) + (warp & 3) * 32;   // the warp's first key
         for (int32_t i = 0; i < it.nt; ++i, ++qit, ++p) {
           const uint32_t st = qit % kQStages;
           // ---- phase A: P = exp2(scale_log2 S - LSE log2 e), P~ = P M / (1-p) -> bf16 over S^T
+          // keep bits of this key row for the warpgroup's 64 query columns (issued before the
+          // waits: the load's latency hides behind them)
+          uint2 kw = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+          if (kDrop == 2 && key_ok)
+            kw = __ldg(prm.mk + (((int64_t)it.h * prm.T + it.c0 + key) * prm.MT + i) * 2 + x);
           TR(1);
           mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);   // LSE / Delta of this query tile
           mbar_wait(&sm.s_full, p & 1);
@@ -406,8 +416,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
               }
           }
           TR(3);
-          uint32_t keep[2] = {0xFFFFFFFFu, 0xFFFFFFFFu};
-          if (kDropout) {
+          uint32_t keep[2] = {kw.x, kw.y};                  // bit e: query 64x + 32ch + e of the tile
+          if (kDrop == 1) {
+            const uint32_t warp_j0 = (uint32_t)(kt * kTile) + (warp & 3) * 32;   // the warp's first key
 #pragma unroll
             for (int ch = 0; ch < 2; ++ch) {
               const uint32_t tq = (uint32_t)(it.c0 + i * kTile + (int)x * 64 + ch * 32);
@@ -711,8 +722,15 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   const bool drop = p.p_dropout > 0.f;
   // plan and item table in shared memory, else the global plan decoded per item
   const bool big = !item_table_fits(p.B, max_items, grid);
-  auto kern = drop ? (big ? bwd::fmha_bwd_kernel<true, true> : bwd::fmha_bwd_kernel<true, false>)
-                   : (big ? bwd::fmha_bwd_kernel<false, true> : bwd::fmha_bwd_kernel<false, false>);
+  // dropout bits: read from the caller's materialised mask (one pass per step shared by both
+  // directions), else regenerated by Philox inside the kernel (cheaper than materialising it
+  // for a single call)
+  const int mode = !drop ? 0 : (p.dropout_mask != nullptr ? 2 : 1);
+  using KernT = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, bwd::Params);
+  static const KernT table[6] = {bwd::fmha_bwd_kernel<0, false>, bwd::fmha_bwd_kernel<0, true>,
+                                 bwd::fmha_bwd_kernel<1, false>, bwd::fmha_bwd_kernel<1, true>,
+                                 bwd::fmha_bwd_kernel<2, false>, bwd::fmha_bwd_kernel<2, true>};
+  const KernT kern = table[mode * 2 + (big ? 1 : 0)];
   {
     const ub_status sa = smem_attr_once(reinterpret_cast<const void*>(kern), (int)bwd::kSmemBytes);
     if (sa != UB_OK) return sa;
@@ -735,6 +753,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
     return st;
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
   if (big && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 0, v, s)) != UB_OK) return st;
+  const void* mask = p.dropout_mask;
   const int64_t rows = p.T * p.heads;
   launch_pdl(bwd::bwd_pre_kernel, dim3((unsigned)((rows * 8 + 255) / 256)), dim3(256), 0, s,
              static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), delta, p.T, p.heads);
@@ -758,6 +777,8 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   prm.k0 = (uint32_t)(p.seed & 0xFFFFFFFFull);
   prm.k1 = (uint32_t)(p.seed >> 32);
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
+  prm.mk = reinterpret_cast<const uint2*>(static_cast<const char*>(mask) + (mask ? dropout_mask_bytes(p) / 2 : 0));
+  prm.MT = mask_tiles(p);
   prof_record(kProfBwd, 0, s);
   launch_pdl(kern, dim3(grid), dim3(bwd::kThreads), bwd::kSmemBytes, s, tq, tdo, tdq, tdkv, prm);
   UB_CHECK_LAUNCH();

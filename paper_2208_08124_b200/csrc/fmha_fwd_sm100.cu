@@ -81,7 +81,7 @@ struct Params {
   int32_t B, H, max_tiles;
   int64_t T;
   float scale, scale_log2;
-  float rp;           // 1 / (1 - p)
+  float rp;           // 1 / (1 - p_eff)
   uint32_t thr, k0, k1, off;
 };
 
@@ -95,10 +95,14 @@ __host__ __device__ constexpr uint32_t col_o(int x) { return 256u * x + 192u; }
 // kPack: 0 = bf16 packing by cvt (XU pipe), 1 = integer rounding + byte permute.
 // kDropout: compile the Philox mask in (p > 0) or out (p == 0: no RNG code at all, so the
 // compiler cannot hoist it into the exp loop).  kBigB: batch larger than the smem plan cache.
-template <int kPoly, int kPack, bool kDropout, bool kBigB>
+// kDrop: 0 no dropout, 1 keep bits by Philox in the softmax loop, 2 keep bits read from the
+// mask ub_dropout_mask materialised (query-major, 16 bytes per thread and key tile)
+template <int kPoly, int kPack, int kDrop, bool kBigB>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_constant__ CUtensorMap tmap_out,
-                const __grid_constant__ CUtensorMap tmap_pad, const Params prm) {
+                const __grid_constant__ CUtensorMap tmap_pad, const Params prm,
+                const uint4* __restrict__ mq,   // dropout keep bits, query-major [H][T][MT] x 128 keys
+                int32_t MT) {
   // Taken straight from the __shared__ array so that every access compiles to LDS/STS (a
   // generic pointer would turn them into long-latency generic loads); the dynamic smem
   // window starts 1024-B aligned (checked), as the 128-B swizzle atoms require.
@@ -109,6 +113,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   const uint32_t lane = lane_id();
   uint32_t tr_n = 0;
   (void)tr_n;
+  constexpr bool kDropout = kDrop != 0;
 
   pdl_launch_dependents();
   if (warp == 10) {                                      // idle warps: the zero block for padded rows
@@ -347,6 +352,13 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       const uint32_t t_glob = (uint32_t)(it.c0 + row);
       float m_run = -INFINITY, l = 0.f;
       for (int32_t j = 0; j < it.nt; ++j) {
+        // keep bits of this key tile's 128 keys (issued before the S wait: its latency hides there)
+        uint32_t kw[4];
+        if constexpr (kDrop == 2) {
+          uint4 w = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+          if (row < it.L) w = __ldg(mq + ((int64_t)it.h * prm.T + t_glob) * MT + j);
+          kw[0] = w.x; kw[1] = w.y; kw[2] = w.z; kw[3] = w.w;
+        }
         TR(1);
         mbar_wait(&sm.s_full[x], s_cnt & 1);
         TR(2);
@@ -393,6 +405,7 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         uint64_t acc2[4] = {0, 0, 0, 0};
         uint32_t pk[kTile / 2];
         uint32_t bits16 = 0;
+        (void)bits16;
 #pragma unroll
         for (int g = 0; g < kTile / 8; ++g) {          // 8 keys at a time: exp2, sum, dropout, pack
           float e8[8];
@@ -411,9 +424,14 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             e8[2 * u] = a;
             e8[2 * u + 1] = b;
           }
-          if (kDropout) {
-            if ((g & 1) == 0) bits16 = keep_bits16(j * kTile + g * 8, t_glob, it.h, prm.off, prm.k0, prm.k1, prm.thr);
-            const uint32_t bits = bits16 >> (8 * (g & 1));
+          if constexpr (kDropout) {
+            uint32_t bits;
+            if constexpr (kDrop == 2) {
+              bits = kw[g >> 2] >> (8 * (g & 3));
+            } else {
+              if ((g & 1) == 0) bits16 = keep_bits16(j * kTile + g * 8, t_glob, it.h, prm.off, prm.k0, prm.k1, prm.thr);
+              bits = bits16 >> (8 * (g & 1));
+            }
 #pragma unroll
             for (int e = 0; e < 8; ++e)
               if (!((bits >> e) & 1u)) e8[e] = 0.f;
@@ -526,10 +544,13 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
   return (v < lo || v > hi) ? dflt : v;
 }
 
+using FwdKern = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params, const uint4*, int32_t);
 template <int P>
-static void (*pick_fwd(bool drop, bool big))(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params) {
-  if (big) return drop ? fwd::fmha_fwd_kernel<P, 0, true, true> : fwd::fmha_fwd_kernel<P, 0, false, true>;
-  return drop ? fwd::fmha_fwd_kernel<P, 0, true, false> : fwd::fmha_fwd_kernel<P, 0, false, false>;
+static FwdKern pick_fwd(int mode, bool big) {
+  static const FwdKern t[6] = {fwd::fmha_fwd_kernel<P, 0, 0, false>, fwd::fmha_fwd_kernel<P, 0, 0, true>,
+                               fwd::fmha_fwd_kernel<P, 0, 1, false>, fwd::fmha_fwd_kernel<P, 0, 1, true>,
+                               fwd::fmha_fwd_kernel<P, 0, 2, false>, fwd::fmha_fwd_kernel<P, 0, 2, true>};
+  return t[mode * 2 + (big ? 1 : 0)];
 }
 
 ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t* d_cu, void* out, float* lse,
@@ -548,7 +569,10 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   // plan and item table in shared memory, else the global plan decoded per item
   const bool drop = p.p_dropout > 0.f, big = !item_table_fits(p.B, max_items, grid);
   const int poly = poly_env < 0 ? (drop ? 0 : 2) : (poly_env >= 2 ? 2 : 0);
-  void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params) = poly == 2 ? pick_fwd<2>(drop, big) : pick_fwd<0>(drop, big);
+  // dropout bits: read from the caller's materialised mask, else regenerated by Philox in
+  // the softmax loop (cheaper than materialising them for a single call)
+  const int mode = !drop ? 0 : (p.dropout_mask != nullptr ? 2 : 1);
+  const FwdKern kern = poly == 2 ? pick_fwd<2>(mode, big) : pick_fwd<0>(mode, big);
   {
     const ub_status sa = smem_attr_once(reinterpret_cast<const void*>(kern), (int)fwd::kSmemBytes);
     if (sa != UB_OK) return sa;
@@ -568,6 +592,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   FmhaPlanView v = fmha_plan_view(ws, p.B);
   const int32_t max_tiles = (p.max_seqlen + kTile - 1) / kTile;
   if (big && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 2, v, s)) != UB_OK) return st;
+  const void* mask = p.dropout_mask;
 
   fwd::Params prm{};
   prm.padded = static_cast<__nv_bfloat16*>(padded);
@@ -589,7 +614,8 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
 
   prof_record(kProfFwd, 0, s);
-  launch_pdl(kern, dim3(grid), dim3(fwd::kThreads), fwd::kSmemBytes, s, tmap, tmap_out, tmap_pad, prm);
+  launch_pdl(kern, dim3(grid), dim3(fwd::kThreads), fwd::kSmemBytes, s, tmap, tmap_out, tmap_pad, prm,
+             static_cast<const uint4*>(mask), mask_tiles(p));
   UB_CHECK_LAUNCH();
   prof_record(kProfFwd, 1, s);
   return UB_OK;

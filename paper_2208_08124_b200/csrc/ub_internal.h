@@ -67,6 +67,12 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
                          const void* dout, const int32_t* d_cu, void* dqkv, void* ws, cudaStream_t s);
 size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p);
 
+// dropout_mask.cu: R5's keep bits, query-major half then key-major half
+size_t dropout_mask_bytes(const ub_fmha_params& p);
+int32_t mask_tiles(const ub_fmha_params& p);
+uint32_t dropout_threshold(float p);
+ub_status launch_dropout_mask(const ub_fmha_params& p, const int32_t* d_cu, void* mask, cudaStream_t s);
+
 ub_status fmha_fwd_simt(const ub_fmha_params& p, const float* qkv, const int32_t* d_cu, float* out,
                         float* lse, cudaStream_t s);
 ub_status fmha_bwd_simt(const ub_fmha_params& p, const float* qkv, const float* out, const float* lse,

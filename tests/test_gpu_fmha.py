@@ -265,3 +265,45 @@ def test_fwd_with_fused_pad(ub, p):
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
     assert torch.equal(padded.view(torch.int16), ref.view(torch.int16))
+
+
+def test_dropout_mask_layouts_match_oracle(ub):
+    """ub_dropout_mask (R5 materialised): both bit layouts equal the oracle's Philox mask
+    bitwise for every (head, query, key) of a batch with sequences of 1..300 tokens."""
+    from oracle import philox
+    L = [300, 1, 33, 128, 129, 64]
+    off = np.concatenate([[0], np.cumsum(L)]).astype(np.int64)
+    T, H, MT, p, seed, offs = int(off[-1]), 3, 3, 0.1, 0x1234_5678_9ABC, 77
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    m = ub.api.dropout_mask(cu, T, H, 384, p, seed, offs)
+    torch.cuda.synchronize()
+    words = m.cpu().numpy().view(np.uint32)
+    half = words.size // 2
+    mq = words[:H * T * MT * 4].reshape(H, T, MT, 4)
+    mk = words[half:half + H * T * MT * 4].reshape(H, T, MT, 4)
+    for b, Lb in enumerate(L):
+        s = int(off[b])
+        nt = (Lb + 127) // 128
+        for h in range(H):
+            keep = philox.keep_mask_block(seed, offs, s, Lb, h, p)          # [query, key]
+            qbits = np.unpackbits(mq[h, s:s + Lb, :nt].reshape(Lb, -1).view(np.uint8), axis=1, bitorder="little")
+            kbits = np.unpackbits(mk[h, s:s + Lb, :nt].reshape(Lb, -1).view(np.uint8), axis=1, bitorder="little")
+            assert np.array_equal(qbits[:, :Lb].astype(bool), keep), (b, h)
+            assert np.array_equal(kbits[:, :Lb].astype(bool), keep.T), (b, h)
+
+
+def test_external_dropout_mask_same_results(ub):
+    """A mask materialised once (ub_dropout_mask) and passed to both directions gives bitwise
+    the results of the calls that materialise it themselves."""
+    L = [512, 300, 45, 129, 1]
+    lengths, off, qkv, dout = make_batch(L, 4, 64, seed=21)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    qd, gd = qkv.cuda(), dout.cuda()
+    T = int(off[-1])
+    o1, l1 = ub.varlen_fmha_fwd(qd, cu, 512, None, 0.1, 9, 3)
+    d1 = ub.varlen_fmha_bwd(qd, o1, l1, gd, cu, 512, None, 0.1, 9, 3)
+    m = ub.api.dropout_mask(cu, T, 4, 512, 0.1, 9, 3)
+    o2, l2 = ub.varlen_fmha_fwd(qd, cu, 512, None, 0.1, 9, 3, dropout_mask=m)
+    d2 = ub.varlen_fmha_bwd(qd, o2, l2, gd, cu, 512, None, 0.1, 9, 3, dropout_mask=m)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2) and torch.equal(d1, d2)
