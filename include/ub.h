@@ -142,9 +142,10 @@ size_t ub_fmha_workspace_bytes(const ub_fmha_params* prm, int is_bwd);
 /* The attention-dropout keep mask of R5 materialised as bits (an input-only operator, P:402:
  * it needs cu_seqlens, seed and offset only, so it can be produced while the batch is still
  * being exchanged, once per step for both directions).  Writes two layouts into d_mask
- * (device, ub_dropout_mask_bytes(prm) bytes, 16-B aligned), MT = ceil(max_seqlen / 128):
- *   query-major words [H][T][MT][4]: bit e of word w = keep(query row t, key 128 kt + 32 w + e)
- *   key-major words   [H][T][MT][4]: bit e of word c = keep(query 128 it + 32 c + e, key row t)
+ * (device, ub_dropout_mask_bytes(prm) bytes, 16-B aligned), MT = ceil(max_seqlen / 128),
+ * 32-bit words with the packed row innermost (coalesced):
+ *   query-major [H][MT][4][T]: bit e of word [h][kt][w][t] = keep(query row t, key 128 kt + 32 w + e)
+ *   key-major   [H][MT][4][T]: bit e of word [h][it][c][t] = keep(query 128 it + 32 c + e, key row t)
  * (t packed rows, keys / queries counted inside the sequence; words of rows past a sequence
  * end are left unwritten).  Needs 1/256 <= p < 1 (UB_ERR_INVALID_ARG); bf16 path.  Async. */
 size_t ub_dropout_mask_bytes(const ub_fmha_params* prm);

@@ -7,9 +7,11 @@
 // row and j the key index inside the sequence; byte (j & 3) of word ((j & 15) >> 2) >= thr
 // keeps (query t, key j).
 //
-// Two layouts, MT = ceil(max_seqlen / 128) key (or query) tiles per row:
-//   query-major  mq[((h * T + t_q) * MT + kt) * 4 + w]: bit e = key kt*128 + 32w + e of query row t_q
-//   key-major    mk[((h * T + t_k) * MT + it) * 4 + c]: bit e = query it*128 + 32c + e of key row t_k
+// Two layouts of 32-bit words, MT = ceil(max_seqlen / 128) key (or query) tiles per row, the
+// packed row index innermost so that 32 consecutive rows' words are 128 contiguous bytes (the
+// writes here and the loads in the kernels are coalesced):
+//   query-major  mq[((h * MT + kt) * 4 + w) * T + t_q]: bit e = key kt*128 + 32w + e of query row t_q
+//   key-major    mk[((h * MT + it) * 4 + c) * T + t_k]: bit e = query it*128 + 32c + e of key row t_k
 // (the forward's softmax thread owns a query row, the backward's compute thread a key row).
 // One warp computes a 32 x 32 block: lane l the 32 keep bits of query l (two Philox calls),
 // then a five-step shuffle transpose hands lane l the 32 bits of key l.
@@ -34,7 +36,7 @@ __global__ void __launch_bounds__(256) dropout_mask_kernel(const int32_t* __rest
     const uint32_t t = (uint32_t)(c0 + q);
     uint32_t x = keep_bits16((uint32_t)j0, t, (uint32_t)h, off, k0, k1, thr) |
                  (keep_bits16((uint32_t)j0 + 16u, t, (uint32_t)h, off, k0, k1, thr) << 16);
-    if (q < L) mq[((int64_t)h * T + c0 + q) * MT * 4 + (kc >> 2) * 4 + (kc & 3)] = x;
+    if (q < L) mq[((int64_t)h * MT * 4 + kc) * T + c0 + q] = x;          // kc = 4 kt + w
     // 32 x 32 bit transpose: row = lane (query), column = bit (key)  ->  row = key
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) {
@@ -44,7 +46,7 @@ __global__ void __launch_bounds__(256) dropout_mask_kernel(const int32_t* __rest
       x = (lane & (uint32_t)s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y & m) << s));
     }
     const int32_t kk = j0 + (int32_t)lane;
-    if (kk < L) mk[((int64_t)h * T + c0 + kk) * MT * 4 + (qc >> 2) * 4 + (qc & 3)] = x;
+    if (kk < L) mk[((int64_t)h * MT * 4 + qc) * T + c0 + kk] = x;        // qc = 4 it + c
   }
 }
 

@@ -1,7 +1,7 @@
 // Varlen FMHA backward on B200 tensor cores (tcgen05 + TMEM + TMA), bf16 in, fp32 accumulate.
 //
 // Chain rule of Eq. (1) per sequence and head; dropout replayed from R5's keep bits,
-// read from the mask ub_dropout_mask materialised (key-major: 8 bytes per thread and pair) or
+// read from the mask ub_dropout_mask materialised (key-major: 2 words per thread and pair) or
 // regenerated here by Philox (R4/R5):
 //   Delta_i = sum_d dO_id O_id                                   (prologue kernel)
 //   S^T = K Q^T, P^T = exp(scale S^T - LSE), dP~^T = V dO^T       (recompute, TMEM)
@@ -108,7 +108,7 @@ struct Params {
   float scale, scale_log2;
   float rp;
   uint32_t thr, k0, k1, off;
-  const uint2* mk;      // dropout keep bits, key-major [H][T][MT] x 128 queries, as 64-bit halves
+  const uint32_t* mk;   // dropout keep bits, key-major [H][MT][4][T] words
   int32_t MT;
 };
 
@@ -382,8 +382,12 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           // keep bits of this key row for the warpgroup's 64 query columns (issued before the
           // waits: the load's latency hides behind them)
           uint2 kw = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
-          if (kDrop == 2 && key_ok)
-            kw = __ldg(prm.mk + (((int64_t)it.h * prm.T + it.c0 + key) * prm.MT + i) * 2 + x);
+          if (kDrop == 2 && key_ok) {
+            // words c = 2x, 2x+1 (queries 64x..64x+63) at ((h MT + i) 4 + c) T + t: a warp's 32 key
+            // rows read 128 contiguous bytes per word
+            const uint32_t* m0 = prm.mk + (((int64_t)it.h * prm.MT + i) * 4 + 2 * x) * prm.T + it.c0 + key;
+            kw = make_uint2(__ldg(m0), __ldg(m0 + prm.T));
+          }
           TR(1);
           mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);   // LSE / Delta of this query tile
           mbar_wait(&sm.s_full, p & 1);
@@ -777,7 +781,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   prm.k0 = (uint32_t)(p.seed & 0xFFFFFFFFull);
   prm.k1 = (uint32_t)(p.seed >> 32);
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
-  prm.mk = reinterpret_cast<const uint2*>(static_cast<const char*>(mask) + (mask ? dropout_mask_bytes(p) / 2 : 0));
+  prm.mk = reinterpret_cast<const uint32_t*>(static_cast<const char*>(mask) + (mask ? dropout_mask_bytes(p) / 2 : 0));
   prm.MT = mask_tiles(p);
   prof_record(kProfBwd, 0, s);
   launch_pdl(kern, dim3(grid), dim3(bwd::kThreads), bwd::kSmemBytes, s, tq, tdo, tdq, tdkv, prm);

@@ -101,7 +101,7 @@ template <int kPoly, int kPack, int kDrop, bool kBigB>
 __global__ void __launch_bounds__(kThreads, 1)
 fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_constant__ CUtensorMap tmap_out,
                 const __grid_constant__ CUtensorMap tmap_pad, const Params prm,
-                const uint4* __restrict__ mq,   // dropout keep bits, query-major [H][T][MT] x 128 keys
+                const uint32_t* __restrict__ mq,   // dropout keep bits, query-major [H][MT][4][T] words
                 int32_t MT) {
   // Taken straight from the __shared__ array so that every access compiles to LDS/STS (a
   // generic pointer would turn them into long-latency generic loads); the dynamic smem
@@ -355,9 +355,11 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         // keep bits of this key tile's 128 keys (issued before the S wait: its latency hides there)
         uint32_t kw[4];
         if constexpr (kDrop == 2) {
-          uint4 w = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
-          if (row < it.L) w = __ldg(mq + ((int64_t)it.h * prm.T + t_glob) * MT + j);
-          kw[0] = w.x; kw[1] = w.y; kw[2] = w.z; kw[3] = w.w;
+          // word w (keys 32w..32w+31 of the tile) at ((h MT + j) 4 + w) T + t: a warp's 32 rows
+          // read 128 contiguous bytes per word
+          const uint32_t* m0 = mq + ((int64_t)it.h * MT + j) * 4 * prm.T + t_glob;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) kw[w] = row < it.L ? __ldg(m0 + (int64_t)w * prm.T) : 0xFFFFFFFFu;
         }
         TR(1);
         mbar_wait(&sm.s_full[x], s_cnt & 1);
@@ -544,7 +546,7 @@ static int env_int(const char* name, int dflt, int lo, int hi) {
   return (v < lo || v > hi) ? dflt : v;
 }
 
-using FwdKern = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params, const uint4*, int32_t);
+using FwdKern = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, fwd::Params, const uint32_t*, int32_t);
 template <int P>
 static FwdKern pick_fwd(int mode, bool big) {
   static const FwdKern t[6] = {fwd::fmha_fwd_kernel<P, 0, 0, false>, fwd::fmha_fwd_kernel<P, 0, 0, true>,
@@ -615,7 +617,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
 
   prof_record(kProfFwd, 0, s);
   launch_pdl(kern, dim3(grid), dim3(fwd::kThreads), fwd::kSmemBytes, s, tmap, tmap_out, tmap_pad, prm,
-             static_cast<const uint4*>(mask), mask_tiles(p));
+             static_cast<const uint32_t*>(mask), mask_tiles(p));
   UB_CHECK_LAUNCH();
   prof_record(kProfFwd, 1, s);
   return UB_OK;

@@ -279,15 +279,17 @@ def test_dropout_mask_layouts_match_oracle(ub):
     torch.cuda.synchronize()
     words = m.cpu().numpy().view(np.uint32)
     half = words.size // 2
-    mq = words[:H * T * MT * 4].reshape(H, T, MT, 4)
-    mk = words[half:half + H * T * MT * 4].reshape(H, T, MT, 4)
+    mq = words[:H * T * MT * 4].reshape(H, MT, 4, T).transpose(0, 3, 1, 2)     # -> [H, T, MT, 4]
+    mk = words[half:half + H * T * MT * 4].reshape(H, MT, 4, T).transpose(0, 3, 1, 2)
     for b, Lb in enumerate(L):
         s = int(off[b])
         nt = (Lb + 127) // 128
         for h in range(H):
             keep = philox.keep_mask_block(seed, offs, s, Lb, h, p)          # [query, key]
-            qbits = np.unpackbits(mq[h, s:s + Lb, :nt].reshape(Lb, -1).view(np.uint8), axis=1, bitorder="little")
-            kbits = np.unpackbits(mk[h, s:s + Lb, :nt].reshape(Lb, -1).view(np.uint8), axis=1, bitorder="little")
+            qbits = np.unpackbits(np.ascontiguousarray(mq[h, s:s + Lb, :nt]).reshape(Lb, -1).view(np.uint8), axis=1,
+                                  bitorder="little")
+            kbits = np.unpackbits(np.ascontiguousarray(mk[h, s:s + Lb, :nt]).reshape(Lb, -1).view(np.uint8), axis=1,
+                                  bitorder="little")
             assert np.array_equal(qbits[:, :Lb].astype(bool), keep), (b, h)
             assert np.array_equal(kbits[:, :Lb].astype(bool), keep.T), (b, h)
 
