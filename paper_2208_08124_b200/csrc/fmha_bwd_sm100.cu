@@ -6,6 +6,8 @@
 //   Delta_i = sum_d dO_id O_id                                   (prologue kernel)
 //   S^T = K Q^T, P^T = exp(scale S^T - LSE), dP~^T = V dO^T       (recompute, TMEM)
 //   P~ = P M/(1-p), dP = dP~ M/(1-p), dS = P (dP - Delta)          (registers)
+//   (with dropout as P' = P/(1-p) from the exp2 argument, P~ = P' M by a packed-pair mask,
+//    dS = P' (dP~ M - Delta (1-p)): no per-element multiply by 1/(1-p))
 //   dV += P~^T dO, dK += dS^T Q   (TMEM, per key tile)             dQ_i = sum_kt dS K
 //   dK *= scale, dQ *= scale (epilogues)
 //
@@ -220,6 +222,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     // ------------------------------------------------------------ Q / dO producer (per pair)
     uint32_t qit = 0;
     WorkItem it;
+    // with dropout the compute warps work with P' = P / (1-p) = exp2(scale_log2 S - LSE log2 e
+    // + log2(1/(1-p))) and Delta' = Delta (1-p): P~ = P' M and dS = P' (dP~ M - Delta')
+    const float lse_add = kDropout ? log2f(prm.rp) : 0.f, delta_mul = kDropout ? 1.f / prm.rp : 1.f;
     UB_ITEMS(r, it) {
       for (int32_t kt = 0; kt < it.nt; ++kt) {
         for (int32_t i = 0; i < it.nt; ++i, ++qit) {
@@ -235,8 +240,8 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             const int32_t k = (int32_t)lane + 32 * u;
             const bool ok = i * kTile + k < it.L;
             const int64_t idx = (int64_t)it.h * prm.T + q0 + k;
-            lv[u] = ok ? -1.4426950408889634f * __ldg(prm.lse + idx) : -INFINITY;
-            dv[u] = ok ? __ldg(prm.delta + idx) : 0.f;
+            lv[u] = ok ? fmaf(-1.4426950408889634f, __ldg(prm.lse + idx), lse_add) : -INFINITY;
+            dv[u] = ok ? __ldg(prm.delta + idx) * delta_mul : 0.f;
           }
           TR(22);
           mbar_wait(&sm.qdo_empty[st], ph ^ 1);
@@ -431,15 +436,18 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           }
           {
             uint32_t pp[32];
+            // pair jj = 4m + i of chunk ch, walked i-major so that each shifted copy of the keep
+            // word keep_mask2 reads is live for 4 consecutive pairs only
 #pragma unroll
-            for (int e = 0; e < 64; e += 2) {
-              float qa = pf[e], qb = pf[e + 1];
-              if (kDropout) {
-                qa = ((keep[e >> 5] >> (e & 31)) & 1u) ? qa * prm.rp : 0.f;
-                qb = ((keep[e >> 5] >> ((e + 1) & 31)) & 1u) ? qb * prm.rp : 0.f;
-              }
-              pp[e / 2] = pack_bf16(qa, qb);
-            }
+            for (int ch = 0; ch < 2; ++ch)
+#pragma unroll
+              for (int i4 = 0; i4 < 4; ++i4)
+#pragma unroll
+                for (int m4 = 0; m4 < 4; ++m4) {
+                  const int jj = 4 * m4 + i4, e = ch * 32 + 2 * jj;
+                  pp[e / 2] = pack_bf16(pf[e], pf[e + 1]);    // P' (dropout) or P
+                  if (kDropout) pp[e / 2] &= keep_mask2(keep[ch], jj);   // P~ = P' M
+                }
             if (warp_partial) {                            // key rows past the sequence end
 #pragma unroll
               for (int e = 0; e < 32; ++e) pp[e] = key_ok ? pp[e] : 0u;
@@ -451,7 +459,7 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           __syncwarp();
           if (lane == 0) mbar_arrive(&sm.p_full);
           TR(4);
-          // ---- phase B: dS = P (dP~ M / (1-p) - Delta) -> bf16 over dP^T and into smem
+          // ---- phase B: dS = P (dP~ M / (1-p) - Delta) = P' (dP~ M - Delta') -> bf16 over dP^T and into smem
           mbar_wait(&sm.dp_full, p & 1);
           TR(5);
           tc_fence_after();
@@ -467,9 +475,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
               for (int e = 0; e < 32; e += 2) {
                 const float2 dl = *reinterpret_cast<const float2*>(&sm.delta[st][x * 64 + ch * 32 + e]);
                 float dpa = __uint_as_float(dr[ch][e]), dpb = __uint_as_float(dr[ch][e + 1]);
-                if (kDropout) {
-                  dpa = ((keep[ch] >> e) & 1u) ? dpa * prm.rp : 0.f;
-                  dpb = ((keep[ch] >> (e + 1)) & 1u) ? dpb * prm.rp : 0.f;
+                if (kDropout) {                             // dS = P' (dP~ M - Delta')
+                  dpa = ((keep[ch] >> e) & 1u) ? dpa : 0.f;
+                  dpb = ((keep[ch] >> (e + 1)) & 1u) ? dpb : 0.f;
                 }
                 float da, db;
                 f2unpack(fmul2(f2pack(pf[ch * 32 + e], pf[ch * 32 + e + 1]), fadd2(f2pack(dpa, dpb), f2pack(-dl.x, -dl.y))),

@@ -426,21 +426,19 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
             e8[2 * u] = a;
             e8[2 * u + 1] = b;
           }
-          if constexpr (kDropout) {
-            uint32_t bits;
-            if constexpr (kDrop == 2) {
-              bits = kw[g >> 2] >> (8 * (g & 3));
-            } else {
-              if ((g & 1) == 0) bits16 = keep_bits16(j * kTile + g * 8, t_glob, it.h, prm.off, prm.k0, prm.k1, prm.thr);
-              bits = bits16 >> (8 * (g & 1));
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              if (!((bits >> e) & 1u)) e8[e] = 0.f;
-          }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             pk[g * 4 + u] = kPack ? pack_bf16_int(e8[2 * u], e8[2 * u + 1]) : pack_bf16(e8[2 * u], e8[2 * u + 1]);
+          if constexpr (kDropout) {                       // P~ = P M on the packed pairs (l sums P)
+            if constexpr (kDrop == 2) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) pk[g * 4 + u] &= keep_mask2(kw[g >> 2], (g & 3) * 4 + u);
+            } else {
+              if ((g & 1) == 0) bits16 = keep_bits16(j * kTile + g * 8, t_glob, it.h, prm.off, prm.k0, prm.k1, prm.thr);
+#pragma unroll
+              for (int u = 0; u < 4; ++u) pk[g * 4 + u] &= keep_mask2(bits16, (g & 1) * 4 + u);
+            }
+          }
         }
         float rs;
         {

@@ -312,6 +312,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// Keep mask of a packed pair: 0xFFFF / 0x0000 in the low half for keep bit 2j of w, in the
+// high half for bit 2j+1.  One prmt in sign-replicate mode (selector nibble bit 3 copies the
+// msb of the selected byte into the whole byte) reads bit 8m+k from byte m of w << (7-k):
+// ANDed with a packed bf16 pair it keeps or zeroes each element (no per-element select).
+// With j a compile-time constant after unrolling, the 8 shifted copies of w are shared by the
+// 16 pairs of a word: 1.5 instructions per pair.
+__device__ __forceinline__ uint32_t keep_mask2(uint32_t w, int j) {
+  const int k = (2 * j) & 7, m = (2 * j) >> 3;
+  const uint32_t sel = (uint32_t)((m | 8) | ((m | 8) << 4) | (((4 + m) | 8) << 8) | (((4 + m) | 8) << 12));
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(w << (7 - k)), "r"(w << (6 - k)), "r"(sel));
+  return d;
+}
 __device__ __forceinline__ float ex2f(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {

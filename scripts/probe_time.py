@@ -4,6 +4,8 @@ import sys
 import os; _R = os.environ.get("UB_ROOT", "/root/repo"); sys.path.insert(0, _R); sys.path.insert(0, _R + "/tests")
 import numpy as np, torch
 import paper_2208_08124_b200 as ub
+from paper_2208_08124_b200 import api as _api
+ub.dropout_mask = _api.dropout_mask
 import synth
 from gpu_util import make_batch
 dist = sys.argv[1] if len(sys.argv) > 1 else "mlperf_like_v0"
@@ -23,9 +25,11 @@ def t(fn, kid, n=20):
     e1.record(); torch.cuda.synchronize()
     ub.api.profile_events(kid)
     return e0.elapsed_time(e1) / n * 1e3, np.median([a.elapsed_time(b) for a, b in evs]) * 1e3
-o, lse = ub.varlen_fmha_fwd(qd, cu, 512, p_dropout=p)
-tf, kf = t(lambda: ub.varlen_fmha_fwd(qd, cu, 512, p_dropout=p, out=o, lse=lse), 0)
-tb, kb = t(lambda: ub.varlen_fmha_bwd(qd, o, lse, gd, cu, 512, p_dropout=p), 1)
+# MASK=1 (default for p > 0): the step's materialised keep bits, as the bench step uses them
+mk = ub.dropout_mask(cu, T, 16, 512, p) if p > 0 and os.environ.get("MASK", "1") == "1" else None
+o, lse = ub.varlen_fmha_fwd(qd, cu, 512, p_dropout=p, dropout_mask=mk)
+tf, kf = t(lambda: ub.varlen_fmha_fwd(qd, cu, 512, p_dropout=p, out=o, lse=lse, dropout_mask=mk), 0)
+tb, kb = t(lambda: ub.varlen_fmha_bwd(qd, o, lse, gd, cu, 512, p_dropout=p, dropout_mask=mk), 1)
 print(f"{dist} p={p} T={T} fwd call {tf:.1f} us kernel {kf:.1f} us ({4*16*64*s2/kf/1e6:.0f} TFLOP/s) | "
       f"bwd call {tb:.1f} us kernel {kb:.1f} us ({8*16*64*s2/kb/1e6:.0f} TFLOP/s strict) | "
       f"fwd+bwd calls {T/(tf+tb):.1f} Mtok/s")
