@@ -197,13 +197,18 @@ __device__ __forceinline__ uint32_t keep_bits16(uint32_t j0, uint32_t t, uint32_
                                                 uint32_t k1, uint32_t thr) {
   const U4 w = philox4x32_10(j0 >> 4, t, h, off, k0, k1);
   const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-  const uint32_t t4 = thr * 0x01010101u;
+  // SWAR r8 >= thr on the 4 bytes of a word, half of it on the FMA pipe (the ALU pipe carries
+  // Philox's XORs): d's byte msb = [r8 & 0x7F >= thr & 0x7F] (bytes (r8 & 0x7F) + 0x80 -
+  // (thr & 0x7F) never borrow); with the msb of r8 and thr that decides r8 >= thr; the four
+  // msbs (bits 7, 15, 23, 31) land on bits 28..31 of one multiply.  Checked against the byte
+  // compare for every (byte, thr) pair.
+  const uint32_t c1 = 0x80808080u - (thr & 0x7Fu) * 0x01010101u;
   uint32_t bits = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    // bytewise r8 >= thr (0xFF / 0x00 per byte), one distinct bit per byte, summed by a multiply
-    const uint32_t m = __vcmpgeu4(words[q], t4) & 0x08040201u;
-    bits |= ((m * 0x01010101u) >> 24) << (4 * q);
+    const uint32_t d = (words[q] & 0x7F7F7F7Fu) + c1;
+    const uint32_t r = (thr & 0x80u) ? (words[q] & d & 0x80808080u) : ((words[q] | d) & 0x80808080u);
+    bits += ((r * 0x00204081u) >> 28) * (1u << (4 * q));
   }
   return bits;
 }
