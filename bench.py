@@ -788,10 +788,22 @@ def gather_bench(wl, peaks, iters=20):
             fn(bufs[k % 3])
         api.profile_events(kid)
         torch.cuda.synchronize()
-        us = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
+        us_iso = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
+        # back to back (how the step runs them): K launches between two events, per launch
+        torch.cuda._sleep(2_000_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(iters):
+            fn(bufs[k % 3])
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / iters * 1e3
         gbs = nbytes / (us * 1e-6) / 1e9
         out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
-                     "bytes": int(nbytes)}
+                     "bytes": int(nbytes), "us_isolated": round(us_iso, 2),
+                     "frac_hbm_isolated": round(nbytes / (us_iso * 1e-6) / 1e9 / peaks["hbm"], 3),
+                     "note": "us: back to back (K launches / K, rotating 3 buffer sets, > L2); us_isolated: "
+                             "median of events recorded right around each launch (includes its ramp)"}
     # the size-matched ceiling: torch's own device copy of the packed tensor (same bytes as unpad;
     # at ~30 MB the launch ramp and drain keep any copy below the 2-GiB copy that measured the peak)
     cp = [torch.empty((T, H * D), dtype=torch.bfloat16, device=wl.dev) for _ in range(3)]

@@ -52,6 +52,53 @@ def test_unpad_pad_bit_exact(ub, row_shape, dtype):
     assert np.array_equal(got2, exp2)
 
 
+@pytest.mark.parametrize("words", [4, 12])
+def test_span_bulk_chunks_cross_sequences(ub, words):
+    # TMA bulk path (16-B rows): 32 KB chunks that hold many short sequences, chunk ends in
+    # the middle of a row (48-B rows), empty sequences in both the packed and the zero space
+    rng = np.random.default_rng(words)
+    lengths = rng.integers(0, 40, 300).astype(np.int32)
+    lengths[[0, 7, 8, 299]] = 0
+    lengths[5] = 512
+    B, S = len(lengths), 512
+    off = np.concatenate([[0], np.cumsum(lengths)])      # (the oracle rejects L = 0, R8: sliced here)
+    T = int(off[-1])
+    padded = rng.integers(-2**31, 2**31 - 1, (B, S, words), dtype=np.int64).astype(np.int32)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    packed = ub.unpad(torch.from_numpy(padded).cuda(), cu, T)
+    exp = np.concatenate([padded[b, :lengths[b]] for b in range(B)])
+    assert np.array_equal(packed.cpu().numpy(), exp)
+    back = ub.pad(packed, cu, B, S).cpu().numpy()
+    ref = np.zeros_like(padded)
+    for b in range(B):
+        ref[b, :lengths[b]] = exp[off[b]:off[b + 1]]
+    assert np.array_equal(back, ref)
+
+
+def test_span_vector_kernel_when_bulk_off():
+    # UB_SPAN_BULK=0 selects the LDG/STG span kernel (read once per process): a subprocess
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, synth\n"
+        "import paper_2208_08124_b200 as ub\n"
+        "from oracle import varlen as ovar\n"
+        "L = synth.gen_lengths('mlperf_like_v0', 56, 9); L[3] = 1\n"
+        "off = ovar.batch_offset(L); T = int(off[-1])\n"
+        "p = torch.randint(0, 255, (56, 512, 64), dtype=torch.uint8)\n"
+        "cu = torch.tensor(off.astype(np.int32)).cuda()\n"
+        "k = ub.unpad(p.cuda(), cu, T)\n"
+        "assert np.array_equal(k.cpu().numpy(), ovar.unpad(p.numpy(), L))\n"
+        "b = ub.pad(k, cu, 56, 512).cpu().numpy()\n"
+        "assert np.array_equal(b, ovar.pad(k.cpu().numpy(), off, 512, np.zeros(64, np.uint8)))\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, UB_SPAN_BULK="0")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
+
+
 def test_unpad_unaligned_and_errors(ub):
     from paper_2208_08124_b200._lib import UbError
     lengths = np.array([3, 1, 4], np.int32)
