@@ -38,7 +38,7 @@ def main(tag):
     summ.setdefault("dram_bytes_per_launch", {})
     summ.setdefault("rounds", {})
     rnd = {}
-    for k in ("fwd", "bwd"):
+    for k in ("fwd", "bwd", "fwd0", "bwd0", "mask"):
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{k}_{tag}.ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -52,8 +52,10 @@ def main(tag):
         rb = float(d["dram__bytes_read.sum"]["value"]) * UNIT.get(d["dram__bytes_read.sum"]["unit"], 1)
         wb = float(d["dram__bytes_write.sum"]["value"]) * UNIT.get(d["dram__bytes_write.sum"]["unit"], 1)
         d["dram_bytes_total"] = rb + wb
-        rnd["fmha_" + k] = d
-        summ["dram_bytes_per_launch"]["fmha_" + k] = rb + wb
+        name = {"fwd": "fmha_fwd", "bwd": "fmha_bwd", "fwd0": "fmha_fwd_p0", "bwd0": "fmha_bwd_p0",
+                "mask": "dropout_mask"}[k]
+        rnd[name] = d
+        summ["dram_bytes_per_launch"][name] = rb + wb
         with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full_{k}_raw.csv"), "w") as f:
             csv.writer(f).writerows(rows)
     # HBM-bound gather kernels (a5 / a6 / a9): one metrics row per launch
@@ -93,7 +95,9 @@ def main(tag):
         rnd["launch_list"] = f"profiles/{tag}_launches.json"
     summ["rounds"][tag] = rnd
     summ["note"] = ("ncu --set full --clock-control none, one launch of each FMHA main kernel from "
-                    "scripts/probe_time.py (config 2 batch); dram bytes are per launch")
+                    "scripts/probe_time.py (config 2 batch; fmha_fwd / fmha_bwd at p = 0.1 with the "
+                    "materialised keep bits -- the headline -- and *_p0 at p = 0 from r02c on); dram bytes "
+                    "are per launch")
     with open(summ_path, "w") as f:
         json.dump(summ, f, indent=1)
     print(json.dumps(rnd, indent=1)[:3000])

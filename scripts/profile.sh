@@ -12,12 +12,18 @@ timeout -k 10 900 python bench.py --steps 30 --warmup 5 > gpurun_out/bench_$TAG.
 timeout -k 10 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu-baseline --no-encoder \
     > gpurun_out/launches_$TAG.log 2>&1
+# the headline configuration: p = 0.1 with the step's materialised keep bits (probe_time.py
+# passes the mask for p > 0); the p = 0 kernels as prof_{fwd,bwd}0_TAG
 for K in fwd bwd; do
   timeout -k 10 900 ncu --set full --clock-control none --import-source on -k regex:fmha_${K}_kernel -s 3 -c 1 \
-      -o gpurun_out/prof_${K}_$TAG -f python scripts/probe_time.py > gpurun_out/ncu_${K}_$TAG.log 2>&1
+      -o gpurun_out/prof_${K}_$TAG -f python scripts/probe_time.py mlperf_like_v0 0.1 > gpurun_out/ncu_${K}_$TAG.log 2>&1
+  timeout -k 10 900 ncu --set full --clock-control none --import-source on -k regex:fmha_${K}_kernel -s 3 -c 1 \
+      -o gpurun_out/prof_${K}0_$TAG -f python scripts/probe_time.py mlperf_like_v0 0.0 > gpurun_out/ncu_${K}0_$TAG.log 2>&1
 done
+timeout -k 10 600 ncu --set full --clock-control none --import-source on -k regex:dropout_mask -s 3 -c 1 \
+    -o gpurun_out/prof_mask_$TAG -f python scripts/probe_mask.py > gpurun_out/ncu_mask_$TAG.log 2>&1
 timeout -k 10 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"span_copy|exchange_copy" -c 15 --csv --log-file gpurun_out/gather_$TAG.csv env PROBE_N=2 python scripts/probe_gather.py \
+    -k regex:"span_copy|span_bulk|exchange_copy" -c 15 --csv --log-file gpurun_out/gather_$TAG.csv env PROBE_N=2 python scripts/probe_gather.py \
     > gpurun_out/gather_$TAG.log 2>&1
 bash scripts/sanitize.sh $TAG > /dev/null 2>&1
 tail -2 gpurun_out/pytest_gpu_$TAG.log; tail -1 gpurun_out/smoke_$TAG.log
