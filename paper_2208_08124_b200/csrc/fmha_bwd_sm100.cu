@@ -179,12 +179,14 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     fence_mbar_init();
   }
   if (warp == 13) tmem_alloc(&sm.tmem_base, 512);
-  pdl_wait();                                            // everything below may read / write global memory
+  // the plan reads only cu_seqlens, which the preceding kernel (bwd_pre) does not write: it is
+  // built before the programmatic-dependency wait, overlapping bwd_pre's tail
   if (!kBigB && warp == 12) {
     build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 0, lane);
     __syncwarp();
     build_item_table(sm.items, sm.plan, prm.cu, prm.B, prm.H, 0, (int32_t)blockIdx.x, (int32_t)gridDim.x, lane);
   }
+  pdl_wait();                                            // everything below may read / write global memory
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -682,32 +684,46 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   }
 }
 
-// Prologue: Delta[h, t] = sum_d O[t,h,d] dO[t,h,d]  (8 threads per (t, h) row, 16-B loads).
+// Prologue: Delta[h, t] = sum_d O[t,h,d] dO[t,h,d]  (8 threads per (t, h) row, 16-B loads,
+// kPreRows rows per thread group so that several loads per thread are in flight).
+constexpr int kPreRows = 4;
 __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __restrict__ out,
                                                       const __nv_bfloat16* __restrict__ dout, float* __restrict__ delta,
                                                       int64_t T, int32_t H) {
   pdl_launch_dependents();
   pdl_wait();                                      // O comes from the forward
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t row = gtid >> 3;                   // (t, h) row
   const int part = (int)(gtid & 7);
-  if (row >= T * H) return;
-  const uint4 a = reinterpret_cast<const uint4*>(out + row * kD)[part];
-  const uint4 b = reinterpret_cast<const uint4*>(dout + row * kD)[part];
-  const uint32_t av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-  float s = 0.f;
+  const int64_t g = gtid >> 3;                     // row group: rows g + k * n_groups
+  const int64_t rows = T * H, n_groups = ((int64_t)gridDim.x * blockDim.x) >> 3;
+  uint4 a[kPreRows], b[kPreRows];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    s = fmaf(__uint_as_float(av[e] << 16), __uint_as_float(bv[e] << 16), s);
-    s = fmaf(__uint_as_float(av[e] & 0xFFFF0000u), __uint_as_float(bv[e] & 0xFFFF0000u), s);
+  for (int k = 0; k < kPreRows; ++k) {
+    const int64_t row = g + k * n_groups;
+    a[k] = b[k] = make_uint4(0, 0, 0, 0);
+    if (row < rows) {
+      a[k] = __ldcs(reinterpret_cast<const uint4*>(out + row * kD) + part);
+      b[k] = __ldcs(reinterpret_cast<const uint4*>(dout + row * kD) + part);
+    }
   }
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  s += __shfl_xor_sync(0xffffffffu, s, 2);
-  s += __shfl_xor_sync(0xffffffffu, s, 4);
-  if (part == 0) {
-    const int64_t t = row / H;
-    const int32_t h = (int32_t)(row - t * H);
-    delta[(int64_t)h * T + t] = s;
+#pragma unroll
+  for (int k = 0; k < kPreRows; ++k) {
+    const int64_t row = g + k * n_groups;
+    const uint32_t av[4] = {a[k].x, a[k].y, a[k].z, a[k].w}, bv[4] = {b[k].x, b[k].y, b[k].z, b[k].w};
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      s = fmaf(__uint_as_float(av[e] << 16), __uint_as_float(bv[e] << 16), s);
+      s = fmaf(__uint_as_float(av[e] & 0xFFFF0000u), __uint_as_float(bv[e] & 0xFFFF0000u), s);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (part == 0 && row < rows) {
+      const int64_t t = row / H;
+      const int32_t h = (int32_t)(row - t * H);
+      delta[(int64_t)h * T + t] = s;
+    }
   }
 }
 
@@ -767,7 +783,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   if (big && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 0, v, s)) != UB_OK) return st;
   const void* mask = p.dropout_mask;
   const int64_t rows = p.T * p.heads;
-  launch_pdl(bwd::bwd_pre_kernel, dim3((unsigned)((rows * 8 + 255) / 256)), dim3(256), 0, s,
+  launch_pdl(bwd::bwd_pre_kernel, dim3((unsigned)((rows * 8 + 256 * bwd::kPreRows - 1) / (256 * bwd::kPreRows))), dim3(256), 0, s,
              static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), delta, p.T, p.heads);
   UB_CHECK_LAUNCH();
 
