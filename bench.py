@@ -292,23 +292,57 @@ def oracle_sample(qkv_cpu, dout_cpu, L, seqs, scale):
     return tok
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((int(i.get("num_threads", 1)) for i in threadpool_info()), default=1)
+    except Exception:
+        return None
+
+
 def cpu_baseline(args, seconds):
     """The oracle as it stands, timed on this host's cores on a bounded sample of the
-    workload (sequences of batch 0 in order, fwd+bwd, until `seconds` elapse)."""
+    workload (sequences of batch 0 in order, fwd+bwd, until `seconds` elapse), and again
+    with its BLAS limited to one thread on a shorter sample."""
     L = synth.gen_lengths(args.dist, B, 100)
     T = int(L.sum())
     qkv = synth.gen_normal((T, 3, H, D), 1000)
     dout = synth.gen_normal((T, H, D), 2000)
     cores = len(os.sched_getaffinity(0))
-    t0 = time.perf_counter()
-    tok, n = 0, 0
-    while n < B and time.perf_counter() - t0 < seconds:
-        tok += oracle_sample(qkv, dout, L, [n], 1 / math.sqrt(D))
-        n += 1
-    dt = time.perf_counter() - t0
-    return {"value": tok / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+
+    def leg(secs):
+        t0 = time.perf_counter()
+        tok, n = 0, 0
+        while n < B and time.perf_counter() - t0 < secs:
+            tok += oracle_sample(qkv, dout, L, [n], 1 / math.sqrt(D))
+            n += 1
+        return tok, n, time.perf_counter() - t0
+
+    tok, n, dt = leg(seconds)
+    one = None
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=1):
+            t1, n1, d1 = leg(max(2.0, seconds / 4))
+        one = {"value": t1 / d1, "sample": f"first {n1} sequences ({t1} tokens), {d1:.1f} s, BLAS limited to 1 thread"}
+    except Exception as e:  # threadpoolctl missing: report without the 1-thread leg
+        one = {"unavailable": str(e)[:120]}
+    return {"value": tok / dt, "unit": "tokens/s", "cores": cores, "blas_threads": _blas_threads(),
+            "cpu_model": _cpu_model(), "kind": "oracle",
             "sample": f"fp64 numpy oracle fwd+bwd on the first {n} of 56 sequences ({tok} tokens) of one "
-                      f"{args.dist} batch, H=16 D=64, {dt:.1f} s"}
+                      f"{args.dist} batch, H=16 D=64, {dt:.1f} s",
+            "one_thread": one}
 
 
 def run_reference(args, world, rank):
@@ -337,7 +371,8 @@ def run_reference(args, world, rank):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"bert_large_fmha_{args.dist}", "batch_per_gpu": B, "heads": H, "head_dim": D,
                        "max_seqlen": S},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "blas_threads": _blas_threads(),
+                             "cpu_model": _cpu_model(), "kind": "oracle",
                              "sample": f"{per_step} sequences per step of one {args.dist} batch, fwd+bwd fp64"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
