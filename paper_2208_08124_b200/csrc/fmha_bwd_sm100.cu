@@ -379,6 +379,17 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
     WorkItem it;
 
     UB_ITEMS(ri, it) {
+      // keep bits of key row kt*128 + r for the warpgroup's 64 query columns of query tile i:
+      // words c = 2x, 2x+1 at ((h MT + i) 4 + c) T + t (a warp's 32 key rows read 128 contiguous
+      // bytes per word), loaded one pair ahead within the item
+      auto load_kw = [&](int32_t kt_, int32_t i_) {
+        const int32_t key_ = kt_ * kTile + (int32_t)r;
+        if (key_ >= it.L) return make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+        const uint32_t* m0 = prm.mk + (((int64_t)it.h * prm.MT + i_) * 4 + 2 * x) * prm.T + it.c0 + key_;
+        return make_uint2(__ldg(m0), __ldg(m0 + prm.T));
+      };
+      uint2 kw_next = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+      if (kDrop == 2) kw_next = load_kw(0, 0);
       for (int32_t kt = 0; kt < it.nt; ++kt) {
         const int32_t key = kt * kTile + (int32_t)r;
         const bool key_ok = key < it.L;
@@ -386,14 +397,10 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
         for (int32_t i = 0; i < it.nt; ++i, ++qit, ++p) {
           const uint32_t st = qit % kQStages;
           // ---- phase A: P = exp2(scale_log2 S - LSE log2 e), P~ = P M / (1-p) -> bf16 over S^T
-          // keep bits of this key row for the warpgroup's 64 query columns (issued before the
-          // waits: the load's latency hides behind them)
-          uint2 kw = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
-          if (kDrop == 2 && key_ok) {
-            // words c = 2x, 2x+1 (queries 64x..64x+63) at ((h MT + i) 4 + c) T + t: a warp's 32 key
-            // rows read 128 contiguous bytes per word
-            const uint32_t* m0 = prm.mk + (((int64_t)it.h * prm.MT + i) * 4 + 2 * x) * prm.T + it.c0 + key;
-            kw = make_uint2(__ldg(m0), __ldg(m0 + prm.T));
+          const uint2 kw = kw_next;
+          if (kDrop == 2) {
+            if (i + 1 < it.nt) kw_next = load_kw(kt, i + 1);
+            else if (kt + 1 < it.nt) kw_next = load_kw(kt + 1, 0);
           }
           TR(1);
           mbar_wait(&sm.qdo_full[st], (qit / kQStages) & 1);   // LSE / Delta of this query tile

@@ -351,15 +351,20 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
       const int32_t row = (it.tile + x) * kTile + (int32_t)r;
       const uint32_t t_glob = (uint32_t)(it.c0 + row);
       float m_run = -INFINITY, l = 0.f;
-      for (int32_t j = 0; j < it.nt; ++j) {
-        // keep bits of this key tile's 128 keys (issued before the S wait: its latency hides there)
-        uint32_t kw[4];
-        if constexpr (kDrop == 2) {
-          // word w (keys 32w..32w+31 of the tile) at ((h MT + j) 4 + w) T + t: a warp's 32 rows
-          // read 128 contiguous bytes per word
-          const uint32_t* m0 = mq + ((int64_t)it.h * MT + j) * 4 * prm.T + t_glob;
+      // keep bits of key tile j's 128 keys: word w (keys 32w..32w+31 of the tile) at
+      // ((h MT + j) 4 + w) T + t, a warp's 32 rows read 128 contiguous bytes per word; loaded one
+      // key tile ahead (an L2 load takes longer than the S wait it used to hide behind)
+      auto load_kw = [&](int32_t j, uint32_t (&w4)[4]) {
+        const uint32_t* m0 = mq + ((int64_t)it.h * MT + j) * 4 * prm.T + t_glob;
 #pragma unroll
-          for (int w = 0; w < 4; ++w) kw[w] = row < it.L ? __ldg(m0 + (int64_t)w * prm.T) : 0xFFFFFFFFu;
+        for (int w = 0; w < 4; ++w) w4[w] = row < it.L ? __ldg(m0 + (int64_t)w * prm.T) : 0xFFFFFFFFu;
+      };
+      uint32_t kw_next[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+      if constexpr (kDrop == 2) load_kw(0, kw_next);
+      for (int32_t j = 0; j < it.nt; ++j) {
+        uint32_t kw[4] = {kw_next[0], kw_next[1], kw_next[2], kw_next[3]};
+        if constexpr (kDrop == 2) {
+          if (j + 1 < it.nt) load_kw(j + 1, kw_next);
         }
         TR(1);
         mbar_wait(&sm.s_full[x], s_cnt & 1);

@@ -10,15 +10,18 @@ import synth
 from gpu_util import make_batch
 which = sys.argv[1] if len(sys.argv) > 1 else "fwd"
 dist = sys.argv[2] if len(sys.argv) > 2 else "mlperf_like_v0"
+pd = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0     # dropout p (with the materialised mask)
 L = synth.gen_lengths(dist, 56, 0)
 lengths, off, qkv, dout = make_batch(L, 16, 64)
 cu = torch.tensor(off.astype(np.int32)).cuda(); qd = qkv.cuda(); gd = dout.cuda()
-o, lse = ub.varlen_fmha_fwd(qd, cu, 512)
+from paper_2208_08124_b200 import api as _api
+mk = _api.dropout_mask(cu, int(off[-1]), 16, 512, pd) if pd > 0 else None
+o, lse = ub.varlen_fmha_fwd(qd, cu, 512, p_dropout=pd, dropout_mask=mk)
 for _ in range(3):
     if which == "fwd":
-        o, lse = ub.varlen_fmha_fwd(qd, cu, 512)
+        o, lse = ub.varlen_fmha_fwd(qd, cu, 512, p_dropout=pd, dropout_mask=mk)
     else:
-        ub.varlen_fmha_bwd(qd, o, lse, gd, cu, 512)
+        ub.varlen_fmha_bwd(qd, o, lse, gd, cu, 512, p_dropout=pd, dropout_mask=mk)
 torch.cuda.synchronize()
 nw = 10 if which == "fwd" else 16
 buf = np.zeros(nw * 1024, dtype=np.uint64)
