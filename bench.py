@@ -568,6 +568,7 @@ def run_ours(args, world, rank, local):
     tokens, lens_used = 0, []
     host_step, host_prep, marks = [], [], []
     step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    wl.comm.set_options(force_nccl=wl.force_nccl, host_profile=True)   # host-only phase clocks
     e0.record(wl.main)
     for k in range(args.steps):
         n = args.warmup + k
@@ -585,6 +586,8 @@ def run_ours(args, world, rank, local):
         host_step.append(h1 - h0)
         host_prep.append(time.perf_counter() - h1)
     step_ev[args.steps].record(wl.main)
+    finish_prof = wl.comm.host_profile()
+    wl.comm.set_options(force_nccl=wl.force_nccl, host_profile=False)
     wl.main.wait_stream(wl.side)      # steady state: the K steps plus the exchange of the next one
     e1.record(wl.main)
     torch.cuda.synchronize()
@@ -699,7 +702,12 @@ def run_ours(args, world, rank, local):
                                               "begin_call"],
                                         [round(1e6 * float(x), 1) for x in np.median(np.array(marks), axis=0)]),
                                     enqueue_compute=round(1e6 * float(np.median(host_step)), 1),
-                                    exchange_calls=round(1e6 * float(np.median(host_prep)), 1))}
+                                    exchange_calls=round(1e6 * float(np.median(host_prep)), 1)),
+           "exchange_finish_host_us": {
+               **{k: (round(v, 1) if isinstance(v, float) else v) for k, v in finish_prof.items()},
+               "note": "mean host us per ub_exchange_finish in the timed steps: wait_lengths is the one host "
+                       "wait (for this slot's all-gathered lengths: the GPU's pace, not host work); the rest is "
+                       "host work (plan, tables, launches)"}}
     if e2e is not None:
         out["e2e"] = e2e
     return out, wl

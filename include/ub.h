@@ -426,7 +426,17 @@ ub_status ub_comm_destroy(void* comm);
  * the default (0) copies the self chunk on the device.  Also set by UB_EXCHANGE_FORCE_NCCL=1
  * at ub_comm_init.  Unknown bits -> UB_ERR_INVALID_ARG. */
 #define UB_COMM_FORCE_NCCL 1
+/* UB_COMM_HOST_PROFILE: accumulate the host time ub_exchange_finish spends per phase (read back
+ * by ub_comm_host_profile; setting it restarts the accumulation).  Also on with
+ * UB_EXCHANGE_TRACE=1, which prints the per-finish means when the communicator is destroyed. */
+#define UB_COMM_HOST_PROFILE 2
 ub_status ub_comm_set_options(void* comm, int32_t flags);
+/* Host microseconds accumulated over the finishes since profiling started, per phase, in
+ * out_us[0..n_out): 0 wait for this slot's lengths (the one host wait: the GPU's pace, not
+ * host work), 1 plan, 2 wait for the previous finish's staging copies, 3 tables,
+ * 4 pack launch, 5 NCCL send/recv enqueue, 6 gather + cu_seqlens launch; *out_finishes = the
+ * number of finishes.  Host-only, no synchronisation. */
+ub_status ub_comm_host_profile(void* comm, double* out_us, int32_t n_out, int64_t* out_finishes);
 /* Number of NCCL calls (all-gathers, sends, receives) this communicator has enqueued so far
  * (host counter; evidence that the collective data plane ran). */
 ub_status ub_comm_nccl_ops(void* comm, int64_t* out);

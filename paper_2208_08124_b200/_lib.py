@@ -77,6 +77,7 @@ SIGNATURES = {
     "ub_comm_destroy": (i32, [vp]),
     "ub_comm_set_options": (i32, [vp, i32]),
     "ub_comm_nccl_ops": (i32, [vp, vp]),
+    "ub_comm_host_profile": (i32, [vp, vp, i32, vp]),
     "ub_allgather_lengths": (i32, [vp, vp, vp, i32, vp]),
     "ub_exchange_workspace_bytes": (sz, [i32, i32, i64, i64, i64]),
     "ub_balance_exchange": (i32, [vp, i32, i32, i32, vp, vp, vp, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp]),

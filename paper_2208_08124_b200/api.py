@@ -523,10 +523,21 @@ class Comm:
         check(lib().ub_comm_init(C.byref(h), C.cast(raw, C.c_void_p), world, rank))
         self.handle, self.world, self.rank = h, world, rank
 
-    def set_options(self, force_nccl: bool = False):
+    def set_options(self, force_nccl: bool = False, host_profile: bool = False):
         """force_nccl: the self chunk and a one-rank all-gather also go through NCCL
-        (UB_COMM_FORCE_NCCL), so the collective data plane runs on one GPU."""
-        check(lib().ub_comm_set_options(self.handle, 1 if force_nccl else 0))
+        (UB_COMM_FORCE_NCCL), so the collective data plane runs on one GPU.  host_profile:
+        accumulate the host time of each exchange-finish phase (UB_COMM_HOST_PROFILE)."""
+        check(lib().ub_comm_set_options(self.handle, (1 if force_nccl else 0) | (2 if host_profile else 0)))
+
+    HOST_PHASES = ("wait_lengths", "plan", "wait_staging", "tables", "pack", "nccl_p2p", "gather_cu")
+
+    def host_profile(self) -> dict:
+        """Mean host microseconds per exchange finish, per phase (ub_comm_host_profile)."""
+        out = (C.c_double * 7)()
+        n = C.c_int64(0)
+        check(lib().ub_comm_host_profile(self.handle, out, 7, C.byref(n)))
+        k = max(int(n.value), 1)
+        return {"finishes": int(n.value), **{name: out[i] / k for i, name in enumerate(self.HOST_PHASES)}}
 
     def nccl_ops(self) -> int:
         """NCCL calls (all-gathers, sends, receives) this communicator has enqueued."""

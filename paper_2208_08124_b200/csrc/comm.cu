@@ -176,8 +176,26 @@ extern "C" ub_status ub_comm_destroy(void* comm) {
 extern "C" ub_status ub_comm_set_options(void* comm, int32_t flags) {
   clear_error();
   UB_REQUIRE(comm, UB_ERR_INVALID_ARG, "null comm");
-  UB_REQUIRE((flags & ~UB_COMM_FORCE_NCCL) == 0, UB_ERR_INVALID_ARG, "unknown option bits 0x%x", flags);
-  static_cast<Comm*>(comm)->force_nccl = (flags & UB_COMM_FORCE_NCCL) != 0;
+  UB_REQUIRE((flags & ~(UB_COMM_FORCE_NCCL | UB_COMM_HOST_PROFILE)) == 0, UB_ERR_INVALID_ARG,
+             "unknown option bits 0x%x", flags);
+  Comm* c = static_cast<Comm*>(comm);
+  c->force_nccl = (flags & UB_COMM_FORCE_NCCL) != 0;
+  if ((flags & UB_COMM_HOST_PROFILE) != 0 && !c->trace) {
+    c->trace = true;                                   // restart the accumulation
+    for (double& t : c->t_phase) t = 0.0;
+    c->n_finish = 0;
+  } else if ((flags & UB_COMM_HOST_PROFILE) == 0) {
+    c->trace = false;
+  }
+  return UB_OK;
+}
+
+extern "C" ub_status ub_comm_host_profile(void* comm, double* out_us, int32_t n_out, int64_t* out_finishes) {
+  clear_error();
+  UB_REQUIRE(comm && out_us && out_finishes && n_out >= 1, UB_ERR_INVALID_ARG, "null pointer");
+  const Comm* c = static_cast<const Comm*>(comm);
+  for (int32_t k = 0; k < n_out; ++k) out_us[k] = k < 7 ? c->t_phase[k] : 0.0;
+  *out_finishes = c->n_finish;
   return UB_OK;
 }
 
