@@ -54,6 +54,7 @@ namespace bwd {
 
 #ifdef UB_TRACE
 __device__ uint64_t g_trace[16 * 1024];
+__device__ uint64_t g_cta_time[2 * 1024];   // per-CTA start / end globaltimer (trace builds)
 #define TR(ev)                                                                                          \
   do {                                                                                                  \
     if (blockIdx.x == 0 && lane == 0 && tr_n < 1024)                                                    \
@@ -152,6 +153,13 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   uint32_t tr_n = 0;
   (void)tr_n;
 
+#ifdef UB_TRACE
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_cta_time[2 * blockIdx.x] = t;
+  }
+#endif
   pdl_launch_dependents();
   if (warp == 12 && lane == 0) {
     tma_prefetch_desc(&tmap_qkv);
@@ -685,6 +693,13 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
 
   tc_fence_before();
   __syncthreads();
+#ifdef UB_TRACE
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_cta_time[2 * blockIdx.x + 1] = t;
+  }
+#endif
   if (warp == 13) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -737,6 +752,9 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
 }  // namespace bwd
 
 #ifdef UB_TRACE
+extern "C" __attribute__((visibility("default"))) int ub_debug_bwd_cta_times(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, bwd::g_cta_time, bytes < sizeof(bwd::g_cta_time) ? bytes : sizeof(bwd::g_cta_time));
+}
 extern "C" __attribute__((visibility("default"))) int ub_debug_bwd_trace(void* host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, bwd::g_trace, bytes < sizeof(bwd::g_trace) ? bytes : sizeof(bwd::g_trace));
 }

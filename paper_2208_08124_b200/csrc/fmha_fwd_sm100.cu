@@ -40,6 +40,7 @@ namespace fwd {
 #ifdef UB_TRACE
 // Debug timeline (trace builds only): CTA 0, lane 0 of every warp records (event, clock64).
 __device__ uint64_t g_trace[10 * 1024];
+__device__ uint64_t g_cta_time[2 * 1024];   // per-CTA start / end globaltimer (trace builds)
 #define TR(ev)                                                                                          \
   do {                                                                                                  \
     if (blockIdx.x == 0 && lane == 0 && tr_n < 1024)                                                    \
@@ -115,6 +116,13 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   (void)tr_n;
   constexpr bool kDropout = kDrop != 0;
 
+#ifdef UB_TRACE
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_cta_time[2 * blockIdx.x] = t;
+  }
+#endif
   pdl_launch_dependents();
   if (warp == 10) {                                      // idle warps: the zero block for padded rows
     for (uint32_t i = lane; i < sizeof(sm.zeros) / 16; i += 32) st_shared_v4(smem_u32(sm.zeros) + 16 * i, 0, 0, 0, 0);
@@ -529,6 +537,13 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   if (warp < 8 && lane == 0) bulk_wait_group0();        // output stores complete before exit
   tc_fence_before();
   __syncthreads();
+#ifdef UB_TRACE
+  if (threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 1024) g_cta_time[2 * blockIdx.x + 1] = t;
+  }
+#endif
   if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -538,6 +553,9 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
 }  // namespace fwd
 
 #ifdef UB_TRACE
+extern "C" __attribute__((visibility("default"))) int ub_debug_fwd_cta_times(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, fwd::g_cta_time, bytes < sizeof(fwd::g_cta_time) ? bytes : sizeof(fwd::g_cta_time));
+}
 extern "C" __attribute__((visibility("default"))) int ub_debug_fwd_trace(void* host, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(host, fwd::g_trace, bytes < sizeof(fwd::g_trace) ? bytes : sizeof(fwd::g_trace));
 }
