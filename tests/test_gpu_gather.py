@@ -193,7 +193,7 @@ def test_nccl_exchange_two_phase_pipelined(ub, force_nccl):
     with the copies or (force_nccl) NCCL itself moving the data."""
     B, rec, srec = 56, 16, 4
     comm = ub.Comm(1, 0)
-    comm.set_options(force_nccl=force_nccl)
+    comm.set_options(force_nccl=force_nccl, host_profile=True)
     side = torch.cuda.Stream()
     batches = []
     for k in range(6):
@@ -225,6 +225,9 @@ def test_nccl_exchange_two_phase_pipelined(ub, force_nccl):
         assert np.array_equal(os_.cpu().numpy(), exp["samples"])
         assert np.array_equal(ocu.cpu().numpy(), exp["cu"])
     assert comm.nccl_ops() == (5 * len(batches) if force_nccl else 0)
+    prof = comm.host_profile()                      # UB_COMM_HOST_PROFILE: one sample per finish
+    assert prof["finishes"] == len(batches)
+    assert all(prof[k] >= 0.0 for k in comm.HOST_PHASES) and prof["plan"] > 0.0
     # misuse: finish without a begin, begin on a busy slot, slot out of range
     d = batches[0]
     with pytest.raises(ub.UbError):
