@@ -806,6 +806,10 @@ def exchange_overlap(args, wl, world, last, step_us):
                     "side-stream events around K x (all-gather, unpad, plan, pack, send/recv, unpack)"}
 
 
+def args_dist(wl):
+    return getattr(wl.args, "dist", "mlperf_like_v0")
+
+
 def gather_bench(wl, peaks, iters=20):
     """a6 / a9 on the config-2 hidden state (bf16 [56, 512, 1024] <-> [T, 1024]), HBM-bound:
     algorithmic bytes unpad = 2*T*row, pad = T*row + B*S*row; 3 rotating buffer sets."""
@@ -865,6 +869,37 @@ def gather_bench(wl, peaks, iters=20):
                                     "frac_hbm": round(2 * T * row / (us * 1e-6) / 1e9 / peaks["hbm"], 3),
                                     "note": "torch copy_ of the packed tensor: the achievable copy rate at this size"}
     out["shape"] = f"hidden [{B}, {S}, {H * D}] bf16 <-> [T={T}, {H * D}]"
+    # the qkv row (6 144 B) and a batch-size sweep of the hidden row (the launch
+    # ramp / drain share shrinks as the copy grows); back to back, 2 rotating buffer sets
+    sweep = {}
+    for nb, rb in ((B, 3 * H * D * 2), (2 * B, H * D * 2), (4 * B, H * D * 2), (8 * B, H * D * 2)):
+        Ls = synth.gen_lengths(args_dist(wl), nb, 7 + nb)
+        offs = np.concatenate([[0], np.cumsum(Ls)]).astype(np.int32)
+        Tn = int(offs[-1])
+        cun = torch.from_numpy(offs).to(wl.dev)
+        sets = [(torch.empty((nb, S, rb), dtype=torch.uint8, device=wl.dev),
+                 torch.empty((Tn, rb), dtype=torch.uint8, device=wl.dev)) for _ in range(2)]
+        res = {}
+        for name, fn, nbytes in (("unpad", lambda b: ub.unpad(b[0], cun, Tn, out=b[1]), 2 * Tn * rb),
+                                 ("pad", lambda b: ub.pad(b[1], cun, nb, S, out=b[0]), Tn * rb + nb * S * rb)):
+            for k in range(2):
+                fn(sets[k])
+            torch.cuda.synchronize()
+            torch.cuda._sleep(2_000_000)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for k in range(iters):
+                fn(sets[k % 2])
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) / iters * 1e3
+            res[name] = {"us": round(us, 2), "frac_hbm": round(nbytes / (us * 1e-6) / 1e9 / peaks["hbm"], 3),
+                         "bytes": int(nbytes)}
+        sweep[f"B{nb}_row{rb}"] = res
+        del sets
+    out["sweep"] = sweep
+    out["sweep_note"] = ("frac_hbm against the measured copy bandwidth (read + write); pad's zero fill is "
+                         "write-only traffic, which can exceed that figure")
     # NEXT-3: the exchange's data movement at SURVEY §8(a) a4's stress record size (a bf16
     # hidden row, 2 kB per token), one rank: the pull gather (one pass) against the NCCL
     # path's pack + unpack copies (two passes; the transport between them is a third)
