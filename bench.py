@@ -82,6 +82,8 @@ def parse():
                          "programmatic-dependent-launch overlap, ~13 us per step) and the per-kernel times come "
                          "from a separate instrumented region of the same steps")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--mask-overlap", type=int, default=1,
+                    help="launch step n+1's dropout mask right behind step n's backward (UB_MASK_OVERLAP_PREVIOUS)")
     ap.add_argument("--reserve-sms", type=int, default=4,
                     help="SMs the persistent FMHA grid leaves to the side-stream exchange (r02c: 0 left the "
                          "side-stream copies no SM while the FMHA kernels ran: 280 vs 214 us per step)")
@@ -408,8 +410,15 @@ class Workload:
         self._begin, self._finish, self._unpad, self._fmha, self._prof_on = {}, {}, {}, {}, False
         self._mask = {}
         self.p = args.p_dropout
-        # R5's keep bits, materialised once per step (ub_dropout_mask) and read by both directions
-        self.mask_buf = torch.empty(ub.api.dropout_mask_bytes(self.cap, H, S), dtype=torch.uint8, device=dev)
+        # R5's keep bits, materialised once per step (ub_dropout_mask) and read by both directions;
+        # two buffers: step n+1's mask is launched right behind step n's backward as an
+        # overlapping dependent (UB_MASK_OVERLAP_PREVIOUS) that fills the SMs the backward's
+        # tail leaves idle, while that backward still reads step n's buffer
+        self.mask_bufs = [torch.empty(ub.api.dropout_mask_bytes(self.cap, H, S), dtype=torch.uint8, device=dev)
+                          for _ in range(2)]
+        self.mask_buf = self.mask_bufs[0]
+        self.mask_overlap = bool(args.mask_overlap)
+        self._mask_issued = set()
         self.dqkv = torch.empty((self.cap, 3, H, D), dtype=torch.bfloat16, device=dev)
         self.padded_out = torch.empty((B, S, H, D), dtype=torch.bfloat16, device=dev)
         # the compute stream at the highest priority, the exchange at the lowest: when an SM
@@ -460,6 +469,7 @@ class Workload:
         T, perm = f()
         ex["T"] = T
         ex["perm"] = perm.copy()
+        ex["n"] = n
         self.ex_ready[e].record(self.side)
         if marks is not None:
             marks.append(time.perf_counter())
@@ -482,24 +492,27 @@ class Workload:
     def bound(self, n):
         """The pre-marshalled FMHA calls of step n's buffers (input set, exchange slot, dqkv)."""
         s, e = n % N_SETS, n % N_EX
-        key = (s, e, self.dqkv.data_ptr(), self.p)
+        mb = n % 2
+        key = (s, e, self.dqkv.data_ptr(), self.p, mb)
         b = self._fmha.get(key)
         if b is None:
             st = self.sets[s]
             b = self._fmha[key] = self.ub.api.BoundFmha(
                 st["qkv"], self.ex[e]["cu"], S, self.out, self.lse_buf, dout=st["dout"], dqkv=self.dqkv,
                 p_dropout=self.p, stream=self.main, num_ctas=self.ctas, padded=self.padded_out,
-                dropout_mask=self.mask_buf if self.p > 0 else None)
+                dropout_mask=self.mask_bufs[mb] if self.p > 0 else None)
         return b
 
-    def mask(self, n):
-        """ub_dropout_mask of step n's exchanged batch (cu_seqlens of its exchange slot)."""
+    def mask(self, n, overlap=False):
+        """ub_dropout_mask of step n's exchanged batch (cu_seqlens of its exchange slot) into
+        buffer n % 2; overlap: UB_MASK_OVERLAP_PREVIOUS (launched right behind step n-1's backward)."""
         e = n % N_EX
-        key = (e, self.p)
+        key = (e, self.p, n % 2, overlap)
         m = self._mask.get(key)
         if m is None:
             m = self._mask[key] = self.ub.api.BoundDropoutMask(self.ex[e]["cu"], self.cap, H, S, self.p,
-                                                               self.mask_buf, stream=self.main)
+                                                               self.mask_bufs[n % 2], stream=self.main,
+                                                               overlap_previous=overlap)
         return m
 
     def step(self, n, prof=None, marks=None):
@@ -507,6 +520,11 @@ class Workload:
         ex = self.ex[n % N_EX]
         T = ex["T"]
         self.main.wait_event(self.ex_ready[n % N_EX])
+        # mask overlap: step n+1's exchange is waited for here, so that nothing separates step
+        # n's backward from step n+1's mask on the stream
+        nxt_ready = self.p > 0 and self.mask_overlap and self.ex[(n + 1) % N_EX].get("n") == n + 1
+        if nxt_ready:
+            self.main.wait_event(self.ex_ready[(n + 1) % N_EX])
         if prof is not None:
             for kid, pair in prof.items():
                 self.ub.api.profile_events(kid, *pair)
@@ -518,14 +536,18 @@ class Workload:
         if marks is not None:
             marks.append(time.perf_counter())
         b = self.bound(n)
-        if self.p > 0:
+        if self.p > 0 and n not in self._mask_issued:
             self.mask(n)(T, 0x2208 + n)                     # keep bits for both directions of this step
+        self._mask_issued.discard(n)
         # a7 + a9: the forward's epilogue also writes the padded copy of O, zeros past
         # each length -- the separate pad pass is gone (ub_varlen_fmha_fwd_pad)
         b.fwd(T, 0x2208 + n)
         if marks is not None:
             marks.append(time.perf_counter())
         b.bwd(T, 0x2208 + n)
+        if nxt_ready:                                       # step n+1's keep bits beside the backward's tail
+            self.mask(n + 1, overlap=True)(self.ex[(n + 1) % N_EX]["T"], 0x2208 + n + 1)
+            self._mask_issued.add(n + 1)
         if marks is not None:
             marks.append(time.perf_counter())
         self.done[n % N_EX].record(self.main)

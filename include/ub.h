@@ -150,6 +150,14 @@ size_t ub_fmha_workspace_bytes(const ub_fmha_params* prm, int is_bwd);
  * end are left unwritten).  Needs 1/256 <= p < 1 (UB_ERR_INVALID_ARG); bf16 path.  Async. */
 size_t ub_dropout_mask_bytes(const ub_fmha_params* prm);
 ub_status ub_dropout_mask(const ub_fmha_params* prm, const int32_t* d_cu, void* d_mask, void* stream);
+/* ub_dropout_mask with flags.  UB_MASK_OVERLAP_PREVIOUS: launched as a programmatic dependent of
+ * the kernel before it on the stream and never waiting for it, so its CTAs fill the SMs that
+ * kernel's tail leaves idle -- the CALLER guarantees that the previous kernel neither writes
+ * d_cu nor reads or writes d_mask (e.g. the previous step's backward reading the other one of
+ * two mask buffers).  Unknown bits -> UB_ERR_INVALID_ARG. */
+#define UB_MASK_OVERLAP_PREVIOUS 1
+ub_status ub_dropout_mask_ex(const ub_fmha_params* prm, const int32_t* d_cu, void* d_mask, int32_t flags,
+                             void* stream);
 
 /* The attention-dropout rate the FMHA kernels apply for a requested p (R5): floor(256 p) / 256
  * with p taken as float32; 0 for p <= 0.  (The Dropout_Add_LayerNorm kernels use 16-bit

@@ -44,6 +44,7 @@ SIGNATURES = {
     "ub_dropout_effective_p": (C.c_double, [f32, i32]),
     "ub_dropout_mask_bytes": (sz, [C.POINTER(FmhaParams)]),
     "ub_dropout_mask": (i32, [C.POINTER(FmhaParams), vp, vp, vp]),
+    "ub_dropout_mask_ex": (i32, [C.POINTER(FmhaParams), vp, vp, i32, vp]),
     "ub_varlen_fmha_fwd": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, vp]),
     "ub_varlen_fmha_fwd_pad": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, i32, vp, vp]),
     "ub_varlen_fmha_bwd": (i32, [C.POINTER(FmhaParams), vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -232,13 +232,15 @@ class BoundDropoutMask:
     """ub_dropout_mask on a fixed output buffer, marshalled once: call with (T, seed).  Size
     the buffer for the largest T (dropout_mask_bytes(cap, ...))."""
 
-    def __init__(self, cu, cap, heads, max_seqlen, p_dropout, out, offset=0, stream=None):
+    def __init__(self, cu, cap, heads, max_seqlen, p_dropout, out, offset=0, stream=None, overlap_previous=False):
+        """overlap_previous: UB_MASK_OVERLAP_PREVIOUS (the caller guarantees the previous kernel on
+        the stream neither writes cu nor touches `out`)."""
         B = cu.numel() - 1
         self.prm = fmha_params(B, cap, max_seqlen, heads, 64, torch.bfloat16, None, p_dropout, 0, offset)
         assert out.numel() >= lib().ub_dropout_mask_bytes(C.byref(self.prm))
         self._keep = (cu, out)
-        self._args = (C.byref(self.prm), _ptr(cu), _ptr(out), _stream(stream))
-        self._f = lib().ub_dropout_mask
+        self._args = (C.byref(self.prm), _ptr(cu), _ptr(out), 1 if overlap_previous else 0, _stream(stream))
+        self._f = lib().ub_dropout_mask_ex
         self.cap = cap
 
     def __call__(self, T: int, seed: int):

@@ -26,10 +26,14 @@ __global__ void __launch_bounds__(256) dropout_mask_kernel(const int32_t* __rest
                                                            int32_t MT, int32_t MQ, uint32_t k0, uint32_t k1,
                                                            uint32_t off, uint32_t thr, uint32_t* __restrict__ mq,
                                                            uint32_t* __restrict__ mk) {
+  pdl_launch_dependents();                        // the forward may be scheduled (it waits for us)
   const int32_t b = blockIdx.x / MQ, qc = blockIdx.x - b * MQ, h = blockIdx.y;
   const int32_t c0 = cu[b], L = cu[b + 1] - c0;
   const int32_t n = (L + 31) / 32;
-  if (qc >= n) return;
+  if (qc >= n) {
+    pdl_wait();
+    return;
+  }
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   for (int32_t kc = (int32_t)warp; kc < n; kc += (int32_t)(blockDim.x >> 5)) {
     const int32_t q = qc * 32 + (int32_t)lane, j0 = kc * 32;
@@ -48,6 +52,9 @@ __global__ void __launch_bounds__(256) dropout_mask_kernel(const int32_t* __rest
     const int32_t kk = j0 + (int32_t)lane;
     if (kk < L) mk[((int64_t)h * MT * 4 + qc) * T + c0 + kk] = x;        // qc = 4 it + c
   }
+  // launched as an overlapping dependent (UB_MASK_OVERLAP_PREVIOUS): finish only after the
+  // previous kernel, so that a kernel waiting for this one also waits for that one
+  pdl_wait();
 }
 
 int32_t mask_tiles(const ub_fmha_params& p) { return (p.max_seqlen + kTile - 1) / kTile; }
@@ -58,16 +65,22 @@ size_t dropout_mask_bytes(const ub_fmha_params& p) {
 
 uint32_t dropout_threshold(float p) { return p > 0.f ? (uint32_t)floor((double)p * 256.0) : 0u; }
 
-ub_status launch_dropout_mask(const ub_fmha_params& p, const int32_t* d_cu, void* mask, cudaStream_t s) {
+ub_status launch_dropout_mask(const ub_fmha_params& p, const int32_t* d_cu, void* mask, cudaStream_t s,
+                              bool overlap_previous) {
   const int32_t MT = mask_tiles(p);
   uint32_t* mq = static_cast<uint32_t*>(mask);
   uint32_t* mk = reinterpret_cast<uint32_t*>(static_cast<char*>(mask) + dropout_mask_bytes(p) / 2);
   const int32_t MQ = (p.max_seqlen + 31) / 32;
   const int64_t nx = (int64_t)p.B * MQ;
   UB_REQUIRE(nx < (1ll << 31), UB_ERR_UNSUPPORTED, "batch too large for the mask launch");
-  dropout_mask_kernel<<<dim3((unsigned)nx, (unsigned)p.heads), 128, 0, s>>>(
-      d_cu, p.heads, p.T, MT, MQ, (uint32_t)(p.seed & 0xFFFFFFFFull), (uint32_t)(p.seed >> 32),
-      (uint32_t)(p.offset & 0xFFFFFFFFull), dropout_threshold(p.p_dropout), mq, mk);
+  const dim3 grid((unsigned)nx, (unsigned)p.heads);
+  const uint32_t k0 = (uint32_t)(p.seed & 0xFFFFFFFFull), k1 = (uint32_t)(p.seed >> 32);
+  const uint32_t off = (uint32_t)(p.offset & 0xFFFFFFFFull), thr = dropout_threshold(p.p_dropout);
+  if (overlap_previous)   // the kernel never waits: it may run beside the previous kernel's tail
+    launch_pdl(dropout_mask_kernel, grid, dim3(128), 0, s, d_cu, (int32_t)p.heads, (int64_t)p.T, MT, MQ, k0, k1, off, thr,
+               mq, mk);
+  else
+    dropout_mask_kernel<<<grid, 128, 0, s>>>(d_cu, p.heads, p.T, MT, MQ, k0, k1, off, thr, mq, mk);
   UB_CHECK_LAUNCH();
   return UB_OK;
 }
@@ -81,8 +94,10 @@ extern "C" size_t ub_dropout_mask_bytes(const ub_fmha_params* p) {
   return dropout_mask_bytes(*p);
 }
 
-extern "C" ub_status ub_dropout_mask(const ub_fmha_params* p, const int32_t* d_cu, void* d_mask, void* stream) {
+extern "C" ub_status ub_dropout_mask_ex(const ub_fmha_params* p, const int32_t* d_cu, void* d_mask, int32_t flags,
+                                       void* stream) {
   clear_error();
+  UB_REQUIRE((flags & ~UB_MASK_OVERLAP_PREVIOUS) == 0, UB_ERR_INVALID_ARG, "unknown flag bits 0x%x", flags);
   UB_REQUIRE(p && d_cu && d_mask, UB_ERR_INVALID_ARG, "null pointer");
   UB_REQUIRE(p->B >= 1 && p->T >= 1 && p->heads >= 1 && p->max_seqlen >= 1, UB_ERR_INVALID_ARG, "bad sizes");
   UB_REQUIRE(p->heads <= 65535, UB_ERR_UNSUPPORTED, "heads above 65535");
@@ -90,5 +105,9 @@ extern "C" ub_status ub_dropout_mask(const ub_fmha_params* p, const int32_t* d_c
              "p_dropout %g: the mask needs 1/256 <= p < 1", (double)p->p_dropout);
   UB_REQUIRE(((uintptr_t)d_mask & 15) == 0, UB_ERR_INVALID_ARG, "mask must be 16-B aligned");
   if (ub_status st = require_sm100(); st != UB_OK) return st;
-  return launch_dropout_mask(*p, d_cu, d_mask, as_stream(stream));
+  return launch_dropout_mask(*p, d_cu, d_mask, as_stream(stream), (flags & UB_MASK_OVERLAP_PREVIOUS) != 0);
+}
+
+extern "C" ub_status ub_dropout_mask(const ub_fmha_params* p, const int32_t* d_cu, void* d_mask, void* stream) {
+  return ub_dropout_mask_ex(p, d_cu, d_mask, 0, stream);
 }

@@ -71,7 +71,8 @@ size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p);
 size_t dropout_mask_bytes(const ub_fmha_params& p);
 int32_t mask_tiles(const ub_fmha_params& p);
 uint32_t dropout_threshold(float p);
-ub_status launch_dropout_mask(const ub_fmha_params& p, const int32_t* d_cu, void* mask, cudaStream_t s);
+ub_status launch_dropout_mask(const ub_fmha_params& p, const int32_t* d_cu, void* mask, cudaStream_t s,
+                              bool overlap_previous = false);
 
 ub_status fmha_fwd_simt(const ub_fmha_params& p, const float* qkv, const int32_t* d_cu, float* out,
                         float* lse, cudaStream_t s);

@@ -309,3 +309,38 @@ def test_external_dropout_mask_same_results(ub):
     d2 = ub.varlen_fmha_bwd(qd, o2, l2, gd, cu, 512, None, 0.1, 9, 3, dropout_mask=m)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2) and torch.equal(d1, d2)
+
+
+def test_overlapped_mask_behind_backward(ub):
+    """UB_MASK_OVERLAP_PREVIOUS: the next step's mask launched right behind a backward that
+    reads the other mask buffer (the bench's step pipeline) equals the plain mask bitwise, and
+    the next step's results are bitwise those with the plain mask."""
+    from paper_2208_08124_b200 import api
+    H = 16
+    L1 = synth.gen_lengths("mlperf_like_v0", 56, 31)
+    L2 = synth.gen_lengths("mlperf_like_v0", 56, 32)
+    _, off1, qkv1, dout1 = make_batch(L1, H, 64, seed=41)
+    _, off2, qkv2, dout2 = make_batch(L2, H, 64, seed=42)
+    cu1, cu2 = (torch.tensor(o.astype(np.int32)).cuda() for o in (off1, off2))
+    T1, T2 = int(off1[-1]), int(off2[-1])
+    q1, g1, q2, g2 = qkv1.cuda(), dout1.cuda(), qkv2.cuda(), dout2.cuda()
+    cap = max(T1, T2)
+    bufs = [torch.zeros(api.dropout_mask_bytes(cap, H, 512), dtype=torch.uint8, device="cuda") for _ in range(2)]
+    m1 = api.BoundDropoutMask(cu1, cap, H, 512, 0.1, bufs[0])
+    m2 = api.BoundDropoutMask(cu2, cap, H, 512, 0.1, bufs[1], overlap_previous=True)
+    m1(T1, 5)
+    o, lse = ub.varlen_fmha_fwd(q1, cu1, 512, None, 0.1, 5, 0, dropout_mask=bufs[0])
+    ub.varlen_fmha_bwd(q1, o, lse, g1, cu1, 512, None, 0.1, 5, 0, dropout_mask=bufs[0])
+    m2(T2, 6)                                            # behind the backward, overlapping its tail
+    o2, l2 = ub.varlen_fmha_fwd(q2, cu2, 512, None, 0.1, 6, 0, dropout_mask=bufs[1])
+    d2 = ub.varlen_fmha_bwd(q2, o2, l2, g2, cu2, 512, None, 0.1, 6, 0, dropout_mask=bufs[1])
+    torch.cuda.synchronize()
+    # (words of rows past a sequence end stay unwritten: both buffers start zeroed)
+    plain = torch.zeros_like(bufs[1])
+    api.BoundDropoutMask(cu2, cap, H, 512, 0.1, plain)(T2, 6)
+    torch.cuda.synchronize()
+    assert torch.equal(bufs[1], plain)
+    o3, l3 = ub.varlen_fmha_fwd(q2, cu2, 512, None, 0.1, 6, 0, dropout_mask=plain)
+    d3 = ub.varlen_fmha_bwd(q2, o3, l3, g2, cu2, 512, None, 0.1, 6, 0, dropout_mask=plain)
+    torch.cuda.synchronize()
+    assert torch.equal(o2, o3) and torch.equal(l2, l3) and torch.equal(d2, d3)
