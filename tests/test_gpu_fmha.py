@@ -95,10 +95,11 @@ def test_bf16_fwd_deterministic_and_single_sequence(ub):
 
 @pytest.mark.parametrize("p", [0.0, 0.1])
 def test_bf16_config2_full_batch_every_sequence(ub, p):
-    """BASELINE config 2 exactly as bench.py runs it (56 x mlperf_like_v0 lengths up to 512,
-    16 heads x 64, bf16, persistent grid), at p = 0 and at BERT-large's attention dropout
-    p = 0.1: EVERY sequence's O, LSE, dQ, dK, dV element by element against the fp64 oracle
-    (per sequence, absolute dropout coordinates), under the BASELINE tolerance."""
+    """BASELINE config 2 (56 x mlperf_like_v0 lengths up to 512, 16 heads x 64, bf16, persistent
+    grid), at p = 0 and at BERT-large's attention dropout p = 0.1: EVERY sequence's O, LSE, dQ,
+    dK, dV element by element against the fp64 oracle (per sequence, absolute dropout
+    coordinates), under the BASELINE tolerance.  (bench.py's launch configuration gives these
+    results bitwise: test_bench_launch_configuration_bitwise.)"""
     L = synth.gen_lengths("mlperf_like_v0", 56, 0)
     seed = 0x2208
     lengths, off, qkv, dout, o, lse, d, scale = _run(ub, L, 16, 64, torch.bfloat16, p=p, seed=seed, max_seqlen=512)
@@ -344,3 +345,37 @@ def test_overlapped_mask_behind_backward(ub):
     d3 = ub.varlen_fmha_bwd(q2, o3, l3, g2, cu2, 512, None, 0.1, 6, 0, dropout_mask=plain)
     torch.cuda.synchronize()
     assert torch.equal(o2, o3) and torch.equal(l2, l3) and torch.equal(d2, d3)
+
+
+def test_bench_launch_configuration_bitwise(ub):
+    """The launch configuration bench.py times -- pre-marshalled BoundFmha on capacity-sized
+    buffers, persistent grid of SMs - 4 CTAs, the forward's fused pad, keep bits materialised
+    once per step by BoundDropoutMask -- gives bitwise the results of the plain calls that
+    test_bf16_config2_full_batch_every_sequence checks against the fp64 oracle (config 2,
+    p = 0.1); the padded copy equals ub_pad of O."""
+    from paper_2208_08124_b200 import api
+    H, S, p, seed = 16, 512, 0.1, 0x2208
+    L = synth.gen_lengths("mlperf_like_v0", 56, 0)
+    lengths, off, qkv, dout, o_ref, lse_ref, d_ref, scale = _run(ub, L, H, 64, torch.bfloat16, p=p, seed=seed,
+                                                                   max_seqlen=S)
+    T, cap = int(off[-1]), int(off[-1]) + 300            # capacity-sized buffers, as the bench's
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    q = torch.zeros((cap, 3, H, 64), dtype=torch.bfloat16, device="cuda"); q[:T] = qkv.cuda()
+    g = torch.zeros((cap, H, 64), dtype=torch.bfloat16, device="cuda"); g[:T] = dout.cuda()
+    out = torch.empty((cap, H, 64), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((H, cap), dtype=torch.float32, device="cuda")
+    dq = torch.empty((cap, 3, H, 64), dtype=torch.bfloat16, device="cuda")
+    padded = torch.full((len(L), S, H, 64), 7.0, dtype=torch.bfloat16, device="cuda")
+    mask = torch.empty(api.dropout_mask_bytes(cap, H, S), dtype=torch.uint8, device="cuda")
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    bm = api.BoundDropoutMask(cu, cap, H, S, p, mask)
+    bf = api.BoundFmha(q, cu, S, out, lse, dout=g, dqkv=dq, p_dropout=p, num_ctas=sms - 4, padded=padded,
+                       dropout_mask=mask)
+    bm(T, seed)
+    bf.fwd(T, seed)
+    bf.bwd(T, seed)
+    torch.cuda.synchronize()
+    lse_v = lse.flatten()[:H * T].view(H, T)               # the bound calls use lse as a dense [H, T]
+    assert torch.equal(out[:T].cpu(), o_ref) and torch.equal(lse_v.cpu(), lse_ref)
+    assert torch.equal(dq[:T].cpu(), d_ref)
+    assert torch.equal(padded, ub.pad(out[:T], cu, len(L), S))
