@@ -976,8 +976,19 @@ def gather_bench(wl, peaks, iters=20):
         torch.cuda.synchronize()
         us = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e3
         gbs = nbytes / (us * 1e-6) / 1e9
+        torch.cuda._sleep(2_000_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(iters):
+            fn(k % 3)
+        e1.record()
+        torch.cuda.synchronize()
+        us_b2b = e0.elapsed_time(e1) / iters * 1e3
         out[name] = {"us": round(us, 2), "GBps": round(gbs, 1), "frac_hbm": round(gbs / peaks["hbm"], 3),
-                     "bytes": int(nbytes), "p_dropout": 0.1}
+                     "bytes": int(nbytes), "p_dropout": 0.1, "us_back_to_back": round(us_b2b, 2),
+                     "frac_hbm_back_to_back": round(nbytes / (us_b2b * 1e-6) / 1e9 / peaks["hbm"], 3),
+                     "note": "us: median of the library's events right around each launch (incl. its ramp); "
+                             "back to back: K launches / K (the bwd's includes its small reduce kernel)"}
     return out
 
 
