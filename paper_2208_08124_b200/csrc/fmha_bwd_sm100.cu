@@ -415,6 +415,28 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
           mbar_wait(&sm.s_full, p & 1);
           TR(2);
           tc_fence_after();
+          if (i * kTile + (int32_t)x * 64 >= it.L) {
+            // this warpgroup's 64 query columns are all past the sequence end (x = 1 on a last
+            // query tile of <= 64 rows): P~ = dS = 0 there, written as zeros over its S^T / dP^T
+            // columns once the MMAs have written them (the A operands of dV / dK); the dQ rows
+            // of these queries are never stored, so the smem dS half is not needed
+            uint32_t z[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) z[e] = 0u;
+            tmem_st32(t_row + kColS + x * 64, z);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.p_full);
+            mbar_wait(&sm.dp_full, p & 1);
+            tc_fence_after();
+            tmem_st32(t_row + kColDP + x * 64, z);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.ds_full);
+            continue;
+          }
           float pf[64];                                     // P (fp32), kept for phase B
           {
             uint32_t sr[2][32];
