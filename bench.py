@@ -84,6 +84,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--mask-overlap", type=int, default=1,
                     help="launch step n+1's dropout mask right behind step n's backward (UB_MASK_OVERLAP_PREVIOUS)")
+    ap.add_argument("--schedule", type=int, default=1,
+                    help="host LPT schedule of the backward's work items (ub_fmha_schedule, from the "
+                         "exchange's lengths, uploaded with the exchange; 2: the forward's too); 0: the "
+                         "kernels' snake deal (same results)")
     ap.add_argument("--reserve-sms", type=int, default=4,
                     help="SMs the persistent FMHA grid leaves to the side-stream exchange (r02c: 0 left the "
                          "side-stream copies no SM while the FMHA kernels ran: 280 vs 214 us per step)")
@@ -434,6 +438,18 @@ class Workload:
         # concurrently with the persistent FMHA kernels (P:376-381 overlap)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.ctas = sms - args.reserve_sms
+        # host LPT schedules of the FMHA work items, one pair per exchange slot: built in finish()
+        # from the lengths the exchange delivered and uploaded on the side stream with it
+        self._sched_calls = {}
+        self.sched_on = args.schedule > 0
+        self.sched_fwd = args.schedule > 1
+        if self.sched_on:
+            nf = ub.api.lib().ub_fmha_schedule_ints(B, H, S, self.ctas, 0)
+            nb = ub.api.lib().ub_fmha_schedule_ints(B, H, S, self.ctas, 1)
+            self.sched_host = [(torch.zeros(nf, dtype=torch.int32).pin_memory(),
+                                torch.zeros(nb, dtype=torch.int32).pin_memory()) for _ in range(N_EX)]
+            self.sched_dev = [(torch.zeros(nf, dtype=torch.int32, device=dev),
+                               torch.zeros(nb, dtype=torch.int32, device=dev)) for _ in range(N_EX)]
         self.force_nccl = args.exchange == "nccl-forced"
         if self.force_nccl:
             self.comm.set_options(force_nccl=True)
@@ -470,6 +486,24 @@ class Workload:
         ex["T"] = T
         ex["perm"] = perm.copy()
         ex["n"] = n
+        if self.sched_on:
+            # the FMHA schedule(s) of the batch the exchange delivered (the library reads the
+            # slot's all-gathered lengths through this finish's perm), uploaded on the side stream
+            # behind the exchange.  No host wait for the previous upload from these pinned
+            # buffers (finish(n - N_EX)'s): the finish above waited for begin(n)'s lengths, queued
+            # on the side stream behind it.
+            sk = key + (id(perm),)
+            fs = self._sched_calls.get(sk)
+            if fs is None:
+                hf, hb = self.sched_host[e]
+                df, db = self.sched_dev[e]
+                fs = [self.comm.bind_fmha_schedule(key[0], perm, B, H, S, self.ctas, True, hb, db, stream=self.side)]
+                if self.sched_fwd:
+                    fs.append(self.comm.bind_fmha_schedule(key[0], perm, B, H, S, self.ctas, False, hf, df,
+                                                           stream=self.side))
+                self._sched_calls[sk] = fs
+            for fn in fs:
+                fn()
         self.ex_ready[e].record(self.side)
         if marks is not None:
             marks.append(time.perf_counter())
@@ -536,6 +570,9 @@ class Workload:
         if marks is not None:
             marks.append(time.perf_counter())
         b = self.bound(n)
+        if self.sched_on:
+            df, db = self.sched_dev[n % N_EX]
+            b.set_schedules(df if self.sched_fwd else None, db)
         if self.p > 0 and n not in self._mask_issued:
             self.mask(n)(T, 0x2208 + n)                     # keep bits for both directions of this step
         self._mask_issued.discard(n)
@@ -704,7 +741,10 @@ def run_ours(args, world, rank, local):
                       "max_seqlen": S, "p_dropout": args.p_dropout,
                       "p_dropout_applied": ub.api.dropout_effective_p(args.p_dropout) if args.p_dropout > 0 else 0.0,
                       "balance": args.balance, "skew": args.skew,
-                      "parallelism": f"dp{world}", "fmha_ctas": wl.ctas, "exchange": args.exchange, "l2": "rotating 3 input sets; per-step working set > L2",
+                      "parallelism": f"dp{world}", "fmha_ctas": wl.ctas,
+                      "fmha_schedule": ("snake (in-kernel)", "bwd: host LPT (ub_fmha_schedule), fwd: snake",
+                                        "host LPT (ub_fmha_schedule)")[min(args.schedule, 2)],
+                      "exchange": args.exchange, "l2": "rotating 3 input sets; per-step working set > L2",
                       "step": "unpad records + exchange (side stream) | dropout keep bits (p > 0), fmha fwd with fused "
                    "pad, bwd (main stream)"},
            "roofline": roofline, "kernels": kernels, "fmha_only_tokens_per_s": round(fmha_only, 1),

@@ -135,9 +135,33 @@ typedef struct {
                          cu_seqlens (device, ub_dropout_mask_bytes), read by the forward and the
                          backward; NULL = the kernels regenerate them by Philox as they go (the
                          same bits: results are bitwise identical either way) */
+  const int32_t* schedule; /* device, NULL = the kernels' own snake deal of the length-bucketed
+                         work items; else the ub_fmha_schedule result for THIS call's direction,
+                         lengths, heads, max_seqlen and grid (results are bitwise identical; only
+                         the makespan changes).  Ignored above 512 sequences; a schedule built for
+                         another grid size falls back to the snake deal */
 } ub_fmha_params;
 
 size_t ub_fmha_workspace_bytes(const ub_fmha_params* prm, int is_bwd);
+
+/* Static schedule of the persistent forward / backward grids (an input-only operator, P:402:
+ * it needs the batch's lengths only, which the padding-exchange planner holds one step ahead,
+ * P:376-381).  Longest-processing-time-first list scheduling of the work items -- backward:
+ * (sequence, head); forward: (sequence, head, pair of 128-row query tiles) -- by an estimated
+ * cost (backward nt^2 + 0.3 nt + 0.5 tile pairs for nt = ceil(L / 128); forward 1.0 (two tiles)
+ * or 0.7 (one) per key step + 0.3), each to the least-loaded of `grid` CTAs (ties: lowest
+ * id), in place of the kernels' snake deal (items longest first, round r dealt in alternating
+ * direction).  Pure host function; deterministic.
+ * h_lengths [B] host (the post-exchange lengths in cu_seqlens order, 0 <= L <= max_seqlen
+ * <= 2048, else UB_ERR_CAPACITY / UB_ERR_UNSUPPORTED); grid = the launch's CTA count (num_ctas,
+ * or the SM count); is_bwd selects the item kind.  Output h_sched (host, int32): [0] = grid,
+ * [1 .. grid+1] = offsets (CTA c owns entries off[c] .. off[c+1] - 1), then the entries:
+ * backward b*H + h, forward (b*H + h)*8 + g (query tiles 2g, 2g+1).  cap_ints >=
+ * ub_fmha_schedule_ints(...) else UB_ERR_SHAPE; a CTA with more than 63 items (the kernels'
+ * table) -> UB_ERR_UNSUPPORTED.  Copy it to the device and pass it as prm->schedule. */
+size_t ub_fmha_schedule_ints(int32_t B, int32_t heads, int32_t max_seqlen, int32_t grid, int32_t is_bwd);
+ub_status ub_fmha_schedule(const int32_t* h_lengths, int32_t B, int32_t heads, int32_t max_seqlen, int32_t grid,
+                           int32_t is_bwd, int32_t* h_sched, size_t cap_ints);
 
 /* The attention-dropout keep mask of R5 materialised as bits (an input-only operator, P:402:
  * it needs cu_seqlens, seed and offset only, so it can be produced while the batch is still
@@ -497,6 +521,21 @@ ub_status ub_exchange_finish(void* comm, int32_t slot, int32_t mode, int32_t B, 
                              int64_t srec_bytes, int64_t capacity_tokens, void* d_out_tokens,
                              void* d_out_samples, int32_t* d_out_cu, int32_t* h_perm, int64_t* h_out_T,
                              void* ws, void* stream);
+/* The W*B all-gathered lengths (rank-major, global id r*B + k) of slot `slot`'s last finished
+ * exchange, copied to h_out (host, W*B int32) -- valid until that slot's next begin.  With the
+ * finish's perm, a rank's post-exchange lengths are h_out[perm[rank*B + k]]: the input of
+ * ub_fmha_schedule for the batch the exchange delivered.  A slot with an unfinished begin, or
+ * B above the communicator's staging, -> UB_ERR_INVALID_ARG / UB_ERR_SHAPE.  Host only. */
+ub_status ub_exchange_slot_lengths(void* comm, int32_t slot, int32_t B, int32_t* h_out);
+/* ub_fmha_schedule of the batch slot `slot`'s last finished exchange delivered to this rank
+ * (lengths h_all[h_perm[rank*B + k]], h_perm = that finish's perm), written to h_sched (host,
+ * pinned if d_sched is given) and, if d_sched is not NULL, copied to d_sched (device,
+ * ub_fmha_schedule_ints ints) on `stream` -- the exchange planner emitting the schedule of the
+ * batch it delivers, one call per direction.  B <= 4096.  Errors as ub_fmha_schedule and
+ * ub_exchange_slot_lengths. */
+ub_status ub_exchange_fmha_schedule(void* comm, int32_t slot, const int32_t* h_perm, int32_t B, int32_t heads,
+                                    int32_t max_seqlen, int32_t grid, int32_t is_bwd, int32_t* h_sched,
+                                    size_t cap_ints, int32_t* d_sched, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -24,7 +24,7 @@ P_i32, P_i64 = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
 class FmhaParams(C.Structure):
     _fields_ = [("B", i32), ("T", i64), ("max_seqlen", i32), ("heads", i32), ("head_dim", i32),
                 ("scale", f32), ("p_dropout", f32), ("seed", u64), ("offset", u64), ("dtype", i32),
-                ("num_ctas", i32), ("dropout_mask", vp)]
+                ("num_ctas", i32), ("dropout_mask", vp), ("schedule", vp)]
 
 
 class EncoderParams(C.Structure):
@@ -41,6 +41,10 @@ SIGNATURES = {
     "ub_unpad": (i32, [vp, vp, vp, i32, i32, i64, i64, vp]),
     "ub_pad": (i32, [vp, vp, vp, i32, i32, i64, i64, vp, vp]),
     "ub_fmha_workspace_bytes": (sz, [C.POINTER(FmhaParams), C.c_int]),
+    "ub_fmha_schedule_ints": (sz, [i32, i32, i32, i32, i32]),
+    "ub_fmha_schedule": (i32, [vp, i32, i32, i32, i32, i32, vp, sz]),
+    "ub_exchange_slot_lengths": (i32, [vp, i32, i32, vp]),
+    "ub_exchange_fmha_schedule": (i32, [vp, i32, vp, i32, i32, i32, i32, i32, vp, sz, vp, vp]),
     "ub_dropout_effective_p": (C.c_double, [f32, i32]),
     "ub_dropout_mask_bytes": (sz, [C.POINTER(FmhaParams)]),
     "ub_dropout_mask": (i32, [C.POINTER(FmhaParams), vp, vp, vp]),

@@ -117,12 +117,27 @@ def pad(packed: torch.Tensor, cu: torch.Tensor, B: int, S: int, pad_row: torch.T
 
 # ------------------------------------------------------------------ varlen FMHA
 def fmha_params(B, T, max_seqlen, heads, head_dim, dtype, scale=None, p_dropout=0.0, seed=0, offset=0,
-                num_ctas=0, dropout_mask=None):
+                num_ctas=0, dropout_mask=None, schedule=None):
     return FmhaParams(B=int(B), T=int(T), max_seqlen=int(max_seqlen), heads=int(heads), head_dim=int(head_dim),
                       scale=float(scale if scale is not None else 1.0 / math.sqrt(head_dim)),
                       p_dropout=float(p_dropout), seed=int(seed), offset=int(offset),
                       dtype=UB_BF16 if dtype == torch.bfloat16 else UB_FP32, num_ctas=int(num_ctas),
-                      dropout_mask=(dropout_mask.data_ptr() if dropout_mask is not None else None))
+                      dropout_mask=(dropout_mask.data_ptr() if dropout_mask is not None else None),
+                      schedule=(schedule.data_ptr() if schedule is not None else None))
+
+
+def fmha_schedule(lengths, heads: int, max_seqlen: int, grid: int, is_bwd: bool, out=None) -> np.ndarray:
+    """ub_fmha_schedule: the host LPT schedule (int32 numpy array) of one direction's work items
+    for a batch with these lengths and a persistent grid of `grid` CTAs; copy it to the device and
+    pass it as schedule=... .  out: a preallocated int32 numpy array (e.g. a pinned tensor's view)."""
+    a = np.ascontiguousarray(np.asarray(lengths, dtype=np.int32).reshape(-1))
+    n = int(lib().ub_fmha_schedule_ints(a.size, heads, max_seqlen, grid, 1 if is_bwd else 0))
+    if out is None:
+        out = np.zeros(n, dtype=np.int32)
+    assert out.dtype == np.int32 and out.flags["C_CONTIGUOUS"]       # size: checked by the library
+    check(lib().ub_fmha_schedule(_np_ptr(a), a.size, heads, max_seqlen, grid, 1 if is_bwd else 0, _np_ptr(out),
+                                 out.size))
+    return out
 
 
 def dropout_mask(cu: torch.Tensor, T: int, heads: int, max_seqlen: int, p_dropout: float, seed=0, offset=0,
@@ -141,14 +156,16 @@ def dropout_mask(cu: torch.Tensor, T: int, heads: int, max_seqlen: int, p_dropou
 
 
 def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=None, p_dropout=0.0, seed=0,
-                    offset=0, out=None, lse=None, stream=None, num_ctas=0, padded=None, dropout_mask=None):
+                    offset=0, out=None, lse=None, stream=None, num_ctas=0, padded=None, dropout_mask=None,
+                    schedule=None):
     """Eq. (1) over packed qkv [T, 3, H, D]; returns (out [T,H,D], lse [H,T] fp32).
     padded: optional [B, S, H, D] tensor that the forward also fills with O in the padded
     layout, zeros past each length (a9 fused into the epilogue, ub_varlen_fmha_fwd_pad)."""
     T, three, H, D = qkv.shape
     assert three == 3
     B = cu.numel() - 1
-    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas, dropout_mask)
+    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas, dropout_mask,
+                      schedule)
     if out is None:
         out = torch.empty((T, H, D), dtype=qkv.dtype, device=qkv.device)
     if lse is None:
@@ -164,11 +181,12 @@ def varlen_fmha_fwd(qkv: torch.Tensor, cu: torch.Tensor, max_seqlen: int, scale=
 
 
 def varlen_fmha_bwd(qkv, out, lse, dout, cu, max_seqlen: int, scale=None, p_dropout=0.0, seed=0, offset=0,
-                    dqkv=None, stream=None, num_ctas=0, dropout_mask=None):
+                    dqkv=None, stream=None, num_ctas=0, dropout_mask=None, schedule=None):
     """Backward of varlen_fmha_fwd; returns dqkv [T, 3, H, D]."""
     T, _, H, D = qkv.shape
     B = cu.numel() - 1
-    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas, dropout_mask)
+    prm = fmha_params(B, T, max_seqlen, H, D, qkv.dtype, scale, p_dropout, seed, offset, num_ctas, dropout_mask,
+                      schedule)
     if dqkv is None:
         dqkv = torch.empty_like(qkv)
     ws = _workspace(lib().ub_fmha_workspace_bytes(C.byref(prm), 1), qkv.device, "fmha_bwd")
@@ -208,6 +226,7 @@ class BoundFmha:
         self._bwd = L.ub_varlen_fmha_bwd
         self._bwd_args = (self._p, _ptr(qkv), _ptr(out), _ptr(lse), _ptr(dout), _ptr(cu), _ptr(dqkv), _ptr(ws_b), st)
         self.cap = cap
+        self._sched = (None, None)
 
     def _set(self, T, seed):
         assert 0 < T <= self.cap
@@ -215,14 +234,22 @@ class BoundFmha:
         if seed is not None:
             self.prm.seed = seed
 
+    def set_schedules(self, fwd_sched=None, bwd_sched=None):
+        """Device int32 tensors from fmha_schedule (fwd / bwd direction) for the next calls, or
+        None for the kernels' snake deal (same results)."""
+        self._sched = (fwd_sched.data_ptr() if fwd_sched is not None else None,
+                       bwd_sched.data_ptr() if bwd_sched is not None else None)
+
     def fwd(self, T: int, seed=None):
         self._set(T, seed)
+        self.prm.schedule = self._sched[0]
         st = self._fwd(*self._fwd_args)
         if st:
             check(st)
 
     def bwd(self, T: int, seed=None):
         self._set(T, seed)
+        self.prm.schedule = self._sched[1]
         st = self._bwd(*self._bwd_args)
         if st:
             check(st)
@@ -626,6 +653,31 @@ class Comm:
                 check(st)
             return T_out.value, perm
         call.keep = keep
+        return call
+
+    def slot_lengths(self, slot: int, B: int, out=None) -> np.ndarray:
+        """ub_exchange_slot_lengths: the W*B all-gathered lengths of the slot's last finished
+        exchange (host int32 array)."""
+        if out is None:
+            out = np.zeros(self.world * B, dtype=np.int32)
+        check(lib().ub_exchange_slot_lengths(self.handle, int(slot), int(B), _np_ptr(out)))
+        return out
+
+    def bind_fmha_schedule(self, slot: int, perm: np.ndarray, B: int, heads: int, max_seqlen: int, grid: int,
+                           is_bwd: bool, h_sched: torch.Tensor, d_sched: torch.Tensor, stream=None):
+        """ub_exchange_fmha_schedule marshalled once: a callable () that builds the FMHA schedule of
+        the batch the slot's last finish delivered (its perm array: bind_finish's, refreshed by
+        each call) into pinned h_sched and uploads it to d_sched on `stream`."""
+        assert perm.dtype == np.int32 and h_sched.is_pinned() and d_sched.is_cuda
+        args = (self.handle, int(slot), _np_ptr(perm), int(B), int(heads), int(max_seqlen), int(grid),
+                1 if is_bwd else 0, _ptr(h_sched), int(h_sched.numel()), _ptr(d_sched), _stream(stream))
+        f = lib().ub_exchange_fmha_schedule
+
+        def call():
+            st = f(*args)
+            if st:
+                check(st)
+        call.keep = (perm, h_sched, d_sched)
         return call
 
     def bind_begin(self, slot: int, d_lengths, capacity_tokens, rec, srec, stream=None):

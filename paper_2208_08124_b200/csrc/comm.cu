@@ -397,6 +397,43 @@ extern "C" ub_status ub_exchange_finish(void* comm, int32_t slot, int32_t mode, 
                          cap, d_out_tokens, d_out_samples, d_out_cu, h_perm, h_out_T, ws, as_stream(stream));
 }
 
+extern "C" ub_status ub_exchange_slot_lengths(void* comm, int32_t slot, int32_t B, int32_t* h_out) {
+  clear_error();
+  UB_REQUIRE(comm && h_out, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(slot >= 0 && slot < UB_EXCHANGE_SLOTS, UB_ERR_INVALID_ARG, "slot %d out of [0, %d)", slot,
+             UB_EXCHANGE_SLOTS);
+  const Comm* c = static_cast<const Comm*>(comm);
+  UB_REQUIRE(B >= 1 && B <= c->cap_B, UB_ERR_SHAPE, "B = %d: the slot holds at most %d per rank", B, c->cap_B);
+  UB_REQUIRE(c->slot_B[slot] == 0, UB_ERR_INVALID_ARG, "slot %d has an unfinished begin", slot);
+  std::memcpy(h_out, c->h_all + (size_t)slot * c->W * c->cap_B, sizeof(int32_t) * (size_t)c->W * B);
+  return UB_OK;
+}
+
+extern "C" ub_status ub_exchange_fmha_schedule(void* comm, int32_t slot, const int32_t* h_perm, int32_t B,
+                                               int32_t heads, int32_t max_seqlen, int32_t grid, int32_t is_bwd,
+                                               int32_t* h_sched, size_t cap_ints, int32_t* d_sched, void* stream) {
+  clear_error();
+  UB_REQUIRE(comm && h_perm && h_sched, UB_ERR_INVALID_ARG, "null pointer");
+  UB_REQUIRE(slot >= 0 && slot < UB_EXCHANGE_SLOTS, UB_ERR_INVALID_ARG, "slot %d out of [0, %d)", slot,
+             UB_EXCHANGE_SLOTS);
+  const Comm* c = static_cast<const Comm*>(comm);
+  UB_REQUIRE(B >= 1 && B <= c->cap_B && B <= 4096, UB_ERR_SHAPE, "B = %d: the slot holds at most %d per rank", B,
+             c->cap_B);
+  UB_REQUIRE(c->slot_B[slot] == 0, UB_ERR_INVALID_ARG, "slot %d has an unfinished begin", slot);
+  const int32_t* all = c->h_all + (size_t)slot * c->W * c->cap_B;
+  int32_t lens[4096];
+  for (int32_t k = 0; k < B; ++k) {
+    const int32_t g = h_perm[(size_t)c->rank * B + k];
+    UB_REQUIRE(g >= 0 && g < c->W * B, UB_ERR_INVALID_ARG, "perm entry %d out of range", g);
+    lens[k] = all[g];
+  }
+  ub_status st = ub_fmha_schedule(lens, B, heads, max_seqlen, grid, is_bwd, h_sched, cap_ints);
+  if (st != UB_OK || d_sched == nullptr) return st;
+  const size_t n = fmha_schedule_ints(B, heads, max_seqlen, grid, is_bwd);
+  UB_CHECK_CUDA(cudaMemcpyAsync(d_sched, h_sched, n * sizeof(int32_t), cudaMemcpyHostToDevice, as_stream(stream)));
+  return UB_OK;
+}
+
 extern "C" ub_status ub_balance_exchange(void* comm, int32_t mode, int32_t B, int32_t max_seqlen,
                                          const int32_t* d_my_lengths, const void* d_my_tokens,
                                          const void* d_my_samples, int64_t rec, int64_t srec, int64_t cap,

@@ -113,6 +113,7 @@ struct Params {
   uint32_t thr, k0, k1, off;
   const uint32_t* mk;   // dropout keep bits, key-major [H][MT][4][T] words
   int32_t MT;
+  const int32_t* sched; // host LPT schedule (ub_fmha_schedule), NULL = snake deal
 };
 
 constexpr uint32_t kIdescS = idesc_bf16_f32(128, 128, 0, 0);     // S^T, dP^T: K-major x K-major
@@ -192,7 +193,9 @@ fmha_bwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   if (!kBigB && warp == 12) {
     build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 0, lane);
     __syncwarp();
-    build_item_table(sm.items, sm.plan, prm.cu, prm.B, prm.H, 0, (int32_t)blockIdx.x, (int32_t)gridDim.x, lane);
+    if (!(prm.sched && build_item_table_sched(sm.items, prm.sched, prm.cu, prm.H, 0, (int32_t)blockIdx.x,
+                                              (int32_t)gridDim.x, lane)))
+      build_item_table(sm.items, sm.plan, prm.cu, prm.B, prm.H, 0, (int32_t)blockIdx.x, (int32_t)gridDim.x, lane);
   }
   pdl_wait();                                            // everything below may read / write global memory
   tc_fence_before();
@@ -854,6 +857,7 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
   prm.mk = reinterpret_cast<const uint32_t*>(static_cast<const char*>(mask) + (mask ? dropout_mask_bytes(p) / 2 : 0));
   prm.MT = mask_tiles(p);
+  prm.sched = big ? nullptr : p.schedule;
   prof_record(kProfBwd, 0, s);
   launch_pdl(kern, dim3(grid), dim3(bwd::kThreads), bwd::kSmemBytes, s, tq, tdo, tdq, tdkv, prm);
   UB_CHECK_LAUNCH();

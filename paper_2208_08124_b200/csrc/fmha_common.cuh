@@ -173,6 +173,34 @@ __device__ __forceinline__ void build_item_table(ItemTable& t, const PlanSmem& p
   if (lane == 0) t.n = count;
 }
 
+// The table from a host schedule (ub_fmha_schedule): sched[0] = grid, sched[1 + c] .. sched[2 + c]
+// the CTA's entry range, entries b*H + h (tiles_per_item 0) or (b*H + h)*8 + g (tile pair g).
+// Returns false (the caller falls back to the snake deal) when the schedule was built for
+// another grid size.  Executed by all 32 lanes of one warp.
+__device__ __forceinline__ bool build_item_table_sched(ItemTable& t, const int32_t* __restrict__ sched,
+                                                       const int32_t* __restrict__ cu, int32_t H, int32_t tiles_per_item,
+                                                       int32_t cta, int32_t G, uint32_t lane) {
+  if (__ldg(sched) != G) return false;
+  const int32_t o0 = __ldg(sched + 1 + cta), n = min(__ldg(sched + 2 + cta) - o0, kItemCap - 1);
+  const int32_t* ent = sched + 2 + G + o0;
+  for (int32_t r = (int32_t)lane; r < n; r += 32) {
+    const int32_t e = __ldg(ent + r);
+    const int32_t bh = tiles_per_item == 0 ? e : (e >> 3), g = tiles_per_item == 0 ? 0 : (e & 7);
+    WorkItem it;
+    it.b = bh / H;
+    it.h = bh - it.b * H;
+    it.c0 = cu[it.b];
+    it.L = cu[it.b + 1] - it.c0;
+    it.nt = (it.L + kTile - 1) / kTile;
+    it.pc0 = 0;
+    it.tile = tiles_per_item == 0 ? 0 : 2 * g;
+    it.ntile = tiles_per_item == 0 ? it.nt : min(2, it.nt - 2 * g);
+    t.it[r] = it;
+  }
+  if (lane == 0) t.n = n;
+  return true;
+}
+
 // item r of this CTA: from the table, or (kBigB) decoded from the global plan.  kTail adds
 // a smem-plan decode for items past a full table -- unreachable while item_table_fits holds,
 // but it changes how ptxas allocates the caller's registers: measured 3.6 % faster for the

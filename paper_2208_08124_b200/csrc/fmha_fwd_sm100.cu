@@ -84,6 +84,7 @@ struct Params {
   float scale, scale_log2;
   float rp;           // 1 / (1 - p_eff)
   uint32_t thr, k0, k1, off;
+  const int32_t* sched;   // host LPT schedule (ub_fmha_schedule), NULL = snake deal
 };
 
 constexpr uint32_t kIdescS = idesc_bf16_f32(128, 128, 0, 0);   // Q (K-major) x K (K-major)
@@ -152,7 +153,9 @@ fmha_fwd_kernel(const __grid_constant__ CUtensorMap tmap_qkv, const __grid_const
   if (!kBigB && warp == 8) {
     build_plan_smem(sm.plan, prm.cu, prm.B, prm.H, prm.max_tiles, 2, lane);
     __syncwarp();
-    build_item_table(sm.items, sm.plan, prm.cu, prm.B, prm.H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, lane);
+    if (!(prm.sched && build_item_table_sched(sm.items, prm.sched, prm.cu, prm.H, 2, (int32_t)blockIdx.x,
+                                              (int32_t)gridDim.x, lane)))
+      build_item_table(sm.items, sm.plan, prm.cu, prm.B, prm.H, 2, (int32_t)blockIdx.x, (int32_t)gridDim.x, lane);
   }
   tc_fence_before();
   __syncthreads();
@@ -635,6 +638,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
   prm.k0 = (uint32_t)(p.seed & 0xFFFFFFFFull);
   prm.k1 = (uint32_t)(p.seed >> 32);
   prm.off = (uint32_t)(p.offset & 0xFFFFFFFFull);
+  prm.sched = big ? nullptr : p.schedule;
 
   prof_record(kProfFwd, 0, s);
   launch_pdl(kern, dim3(grid), dim3(fwd::kThreads), fwd::kSmemBytes, s, tmap, tmap_out, tmap_pad, prm,

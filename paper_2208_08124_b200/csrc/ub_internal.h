@@ -66,6 +66,7 @@ ub_status fmha_fwd_sm100(const ub_fmha_params& p, const void* qkv, const int32_t
 ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* out, const float* lse,
                          const void* dout, const int32_t* d_cu, void* dqkv, void* ws, cudaStream_t s);
 size_t fmha_bwd_sm100_ws_bytes(const ub_fmha_params& p);
+size_t fmha_schedule_ints(int32_t B, int32_t H, int32_t max_seqlen, int32_t grid, int32_t is_bwd);
 
 // dropout_mask.cu: R5's keep bits, query-major half then key-major half
 size_t dropout_mask_bytes(const ub_fmha_params& p);

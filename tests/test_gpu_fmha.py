@@ -352,7 +352,7 @@ def test_overlapped_mask_behind_backward(ub):
 def test_bench_launch_configuration_bitwise(ub):
     """The launch configuration bench.py times -- pre-marshalled BoundFmha on capacity-sized
     buffers, persistent grid of SMs - 4 CTAs, the forward's fused pad, keep bits materialised
-    once per step by BoundDropoutMask -- gives bitwise the results of the plain calls that
+    once per step by BoundDropoutMask, host LPT schedules of the work items -- gives bitwise the results of the plain calls that
     test_bf16_config2_full_batch_every_sequence checks against the fp64 oracle (config 2,
     p = 0.1); the padded copy equals ub_pad of O."""
     from paper_2208_08124_b200 import api
@@ -373,6 +373,9 @@ def test_bench_launch_configuration_bitwise(ub):
     bm = api.BoundDropoutMask(cu, cap, H, S, p, mask)
     bf = api.BoundFmha(q, cu, S, out, lse, dout=g, dqkv=dq, p_dropout=p, num_ctas=sms - 4, padded=padded,
                        dropout_mask=mask)
+    # the host LPT schedules the bench uploads with each exchange (ub_fmha_schedule)
+    bf.set_schedules(torch.from_numpy(api.fmha_schedule(lengths, H, S, sms - 4, False)).cuda(),
+                     torch.from_numpy(api.fmha_schedule(lengths, H, S, sms - 4, True)).cuda())
     bm(T, seed)
     bf.fwd(T, seed)
     bf.bwd(T, seed)
@@ -381,3 +384,36 @@ def test_bench_launch_configuration_bitwise(ub):
     assert torch.equal(out[:T].cpu(), o_ref) and torch.equal(lse_v.cpu(), lse_ref)
     assert torch.equal(dq[:T].cpu(), d_ref)
     assert torch.equal(padded, ub.pad(out[:T], cu, len(L), S))
+
+
+@pytest.mark.parametrize("case", ["config2", "edges"])
+def test_host_schedule_same_results(ub, case):
+    """ub_fmha_schedule (host LPT deal of the work items) passed as prm->schedule: forward and
+    backward results bitwise those of the kernels' own snake deal, at p = 0 and 0.1 (with the
+    materialised mask); a schedule built for another grid size falls back to the snake deal."""
+    from paper_2208_08124_b200 import api
+    S = 512
+    if case == "config2":
+        H = 16
+        L = synth.gen_lengths("mlperf_like_v0", 56, 7)
+        G = torch.cuda.get_device_properties(0).multi_processor_count - 4
+    else:
+        H, G = 2, 8
+        L = np.array([1, 127, 128, 129, 300, 512, 64, 65, 449], np.int32)
+    lengths, off, qkv, dout = make_batch(L, H, 64, seed=71)
+    cu = torch.tensor(off.astype(np.int32)).cuda()
+    T = int(off[-1])
+    q, g = qkv.cuda(), dout.cuda()
+    sf = torch.from_numpy(api.fmha_schedule(lengths, H, S, G, False)).cuda()
+    sb = torch.from_numpy(api.fmha_schedule(lengths, H, S, G, True)).cuda()
+    wrong = torch.from_numpy(api.fmha_schedule(lengths, H, S, G - 1, True)).cuda()
+    for p in (0.0, 0.1):
+        m = api.dropout_mask(cu, T, H, S, p, 3, 0) if p > 0 else None
+        o1, l1 = ub.varlen_fmha_fwd(q, cu, S, None, p, 3, 0, num_ctas=G, dropout_mask=m)
+        d1 = ub.varlen_fmha_bwd(q, o1, l1, g, cu, S, None, p, 3, 0, num_ctas=G, dropout_mask=m)
+        o2, l2 = ub.varlen_fmha_fwd(q, cu, S, None, p, 3, 0, num_ctas=G, dropout_mask=m, schedule=sf)
+        d2 = ub.varlen_fmha_bwd(q, o2, l2, g, cu, S, None, p, 3, 0, num_ctas=G, dropout_mask=m, schedule=sb)
+        d3 = ub.varlen_fmha_bwd(q, o2, l2, g, cu, S, None, p, 3, 0, num_ctas=G, dropout_mask=m, schedule=wrong)
+        torch.cuda.synchronize()
+        assert torch.equal(o1, o2) and torch.equal(l1, l2), p
+        assert torch.equal(d1, d2) and torch.equal(d1, d3), p

@@ -240,3 +240,35 @@ def test_nccl_exchange_two_phase_pipelined(ub, force_nccl):
     comm.exchange_finish(3, B, d[4], d[5], cap, 512, "paper", *outs[0], stream=side)
     side.synchronize()
     comm.close()
+
+
+@pytest.mark.gpu
+def test_exchange_emits_fmha_schedule(ub):
+    """ub_exchange_slot_lengths / ub_exchange_fmha_schedule: after a finish, the slot's all-gathered
+    lengths are the batch's, and the schedule the exchange emits (host copy and its upload) is
+    ub_fmha_schedule of the delivered batch's lengths (perm order)."""
+    from paper_2208_08124_b200 import api
+    B, rec, srec, H, S, G = 56, 16, 4, 16, 512, 144
+    lens = synth.gen_lengths("mlperf_like_v0", B, 77)
+    comm = ub.Comm(1, 0)
+    side = torch.cuda.Stream()
+    cap = int(lens.sum())
+    dl = torch.from_numpy(lens).cuda()
+    toks = torch.zeros((cap, rec), dtype=torch.uint8, device="cuda")
+    smps = torch.zeros((B, srec), dtype=torch.uint8, device="cuda")
+    outs = (torch.empty((cap, rec), dtype=torch.uint8, device="cuda"), torch.empty((B, srec), dtype=torch.uint8,
+            device="cuda"), torch.empty(B + 1, dtype=torch.int32, device="cuda"))
+    comm.exchange_begin(2, dl, cap, rec, srec, stream=side)
+    T, perm = comm.exchange_finish(2, B, toks, smps, cap, S, "paper", *outs, stream=side)
+    perm = np.ascontiguousarray(perm, dtype=np.int32)
+    assert np.array_equal(comm.slot_lengths(2, B), lens)
+    delivered = lens[perm[:B]]
+    for is_bwd in (True, False):
+        n = api.lib().ub_fmha_schedule_ints(B, H, S, G, 1 if is_bwd else 0)
+        hs = torch.zeros(n, dtype=torch.int32).pin_memory()
+        ds = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+        comm.bind_fmha_schedule(2, perm, B, H, S, G, is_bwd, hs, ds, stream=side)()
+        side.synchronize()
+        exp = api.fmha_schedule(delivered, H, S, G, is_bwd)
+        assert np.array_equal(hs.numpy(), exp) and np.array_equal(ds.cpu().numpy(), exp)
+    comm.close()
