@@ -88,9 +88,10 @@ def parse():
                     help="host LPT schedule of the backward's work items (ub_fmha_schedule, from the "
                          "exchange's lengths, uploaded with the exchange; 2: the forward's too); 0: the "
                          "kernels' snake deal (same results)")
-    ap.add_argument("--reserve-sms", type=int, default=4,
+    ap.add_argument("--reserve-sms", type=int, default=1,
                     help="SMs the persistent FMHA grid leaves to the side-stream exchange (r02c: 0 left the "
-                         "side-stream copies no SM while the FMHA kernels ran: 280 vs 214 us per step)")
+                         "side-stream copies no SM while the FMHA kernels ran: 280 vs 214 us per step; with "
+                         "the backward's LPT schedule 1 / 2 / 4: median step 219 / 222 / 222 us)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "nccl-forced"],
                     help="nccl-forced: the self chunk / one-rank all-gather also go through NCCL (UB_COMM_FORCE_NCCL)")
     return ap.parse_args()
