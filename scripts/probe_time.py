@@ -29,7 +29,13 @@ def t(fn, kid, n=20):
 mk = ub.dropout_mask(cu, T, 16, 512, p) if p > 0 and os.environ.get("MASK", "1") == "1" else None
 o, lse = ub.varlen_fmha_fwd(qd, cu, 512, p_dropout=p, dropout_mask=mk)
 tf, kf = t(lambda: ub.varlen_fmha_fwd(qd, cu, 512, p_dropout=p, out=o, lse=lse, dropout_mask=mk), 0)
-tb, kb = t(lambda: ub.varlen_fmha_bwd(qd, o, lse, gd, cu, 512, p_dropout=p, dropout_mask=mk), 1)
+# the backward with the host LPT schedule of its work items (as the bench step runs it; SCHED=0: the
+# kernels' snake deal)
+sb = None
+if os.environ.get("SCHED", "1") == "1":
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    sb = torch.from_numpy(_api.fmha_schedule(L, 16, 512, sms, True)).cuda()
+tb, kb = t(lambda: ub.varlen_fmha_bwd(qd, o, lse, gd, cu, 512, p_dropout=p, dropout_mask=mk, schedule=sb), 1)
 print(f"{dist} p={p} T={T} fwd call {tf:.1f} us kernel {kf:.1f} us ({4*16*64*s2/kf/1e6:.0f} TFLOP/s) | "
       f"bwd call {tb:.1f} us kernel {kb:.1f} us ({8*16*64*s2/kb/1e6:.0f} TFLOP/s strict) | "
       f"fwd+bwd calls {T/(tf+tb):.1f} Mtok/s")
