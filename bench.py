@@ -63,7 +63,7 @@ KERNELS_PER_STEP = 5    # ours at W = 1: unpad, exchange gather, fwd main (+ fus
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)   # 100 steps of ~0.23 ms: a stable mean
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--dist", default="mlperf_like_v0", choices=list(synth.DISTRIBUTIONS))
