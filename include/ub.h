@@ -513,7 +513,7 @@ ub_status ub_balance_exchange(void* comm, int32_t mode, int32_t B, int32_t max_s
  *   Issue the begin of step n+1 one step before its finish: by then its event has fired
  *   and the wait is free.  Outputs, capacity and errors as ub_balance_exchange.
  * Collective calls: every rank issues the same begin/finish sequence. */
-#define UB_EXCHANGE_SLOTS 4
+#define UB_EXCHANGE_SLOTS 8
 ub_status ub_exchange_begin(void* comm, int32_t slot, int32_t B, const int32_t* d_my_lengths, void* ws,
                             void* stream);
 ub_status ub_exchange_finish(void* comm, int32_t slot, int32_t mode, int32_t B, int32_t max_seqlen,

@@ -606,7 +606,7 @@ class Comm:
                                         C.byref(T_out), _ptr(ws), _stream(stream)))
         return out_tokens, out_samples, out_cu, int(T_out.value), perm
 
-    SLOTS = 4    # UB_EXCHANGE_SLOTS
+    SLOTS = 8    # UB_EXCHANGE_SLOTS
 
     def _ws(self, B, capacity_tokens, rec, srec, dev):
         return _workspace(lib().ub_exchange_workspace_bytes(self.world, B, capacity_tokens, rec, srec), dev,
@@ -653,6 +653,7 @@ class Comm:
                 check(st)
             return T_out.value, perm
         call.keep = keep
+        call.perm = perm                                 # the array each call refreshes
         return call
 
     def slot_lengths(self, slot: int, B: int, out=None) -> np.ndarray:
