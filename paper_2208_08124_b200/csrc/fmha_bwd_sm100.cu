@@ -741,35 +741,39 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(const __nv_bfloat16* __res
   pdl_wait();                                      // O comes from the forward
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int part = (int)(gtid & 7);
-  const int64_t g = gtid >> 3;                     // row group: rows g + k * n_groups
+  const int64_t g = gtid >> 3;                     // row group: rows base + g + k * n_groups
   const int64_t rows = T * H, n_groups = ((int64_t)gridDim.x * blockDim.x) >> 3;
-  uint4 a[kPreRows], b[kPreRows];
+  // grid-stride over blocks of kPreRows * n_groups rows: a one-wave grid (host) keeps every SM
+  // streaming to the end instead of a partial last wave
+  for (int64_t base = 0; base < rows; base += kPreRows * n_groups) {
+    uint4 a[kPreRows], b[kPreRows];
 #pragma unroll
-  for (int k = 0; k < kPreRows; ++k) {
-    const int64_t row = g + k * n_groups;
-    a[k] = b[k] = make_uint4(0, 0, 0, 0);
-    if (row < rows) {
-      a[k] = __ldcs(reinterpret_cast<const uint4*>(out + row * kD) + part);
-      b[k] = __ldcs(reinterpret_cast<const uint4*>(dout + row * kD) + part);
+    for (int k = 0; k < kPreRows; ++k) {
+      const int64_t row = base + g + k * n_groups;
+      a[k] = b[k] = make_uint4(0, 0, 0, 0);
+      if (row < rows) {
+        a[k] = __ldcs(reinterpret_cast<const uint4*>(out + row * kD) + part);
+        b[k] = __ldcs(reinterpret_cast<const uint4*>(dout + row * kD) + part);
+      }
     }
-  }
 #pragma unroll
-  for (int k = 0; k < kPreRows; ++k) {
-    const int64_t row = g + k * n_groups;
-    const uint32_t av[4] = {a[k].x, a[k].y, a[k].z, a[k].w}, bv[4] = {b[k].x, b[k].y, b[k].z, b[k].w};
-    float s = 0.f;
+    for (int k = 0; k < kPreRows; ++k) {
+      const int64_t row = base + g + k * n_groups;
+      const uint32_t av[4] = {a[k].x, a[k].y, a[k].z, a[k].w}, bv[4] = {b[k].x, b[k].y, b[k].z, b[k].w};
+      float s = 0.f;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      s = fmaf(__uint_as_float(av[e] << 16), __uint_as_float(bv[e] << 16), s);
-      s = fmaf(__uint_as_float(av[e] & 0xFFFF0000u), __uint_as_float(bv[e] & 0xFFFF0000u), s);
-    }
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    if (part == 0 && row < rows) {
-      const int64_t t = row / H;
-      const int32_t h = (int32_t)(row - t * H);
-      delta[(int64_t)h * T + t] = s;
+      for (int e = 0; e < 4; ++e) {
+        s = fmaf(__uint_as_float(av[e] << 16), __uint_as_float(bv[e] << 16), s);
+        s = fmaf(__uint_as_float(av[e] & 0xFFFF0000u), __uint_as_float(bv[e] & 0xFFFF0000u), s);
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      s += __shfl_xor_sync(0xffffffffu, s, 4);
+      if (part == 0 && row < rows) {
+        const int64_t t = row / H;
+        const int32_t h = (int32_t)(row - t * H);
+        delta[(int64_t)h * T + t] = s;
+      }
     }
   }
 }
@@ -833,7 +837,19 @@ ub_status fmha_bwd_sm100(const ub_fmha_params& p, const void* qkv, const void* o
   if (big && (st = launch_fmha_plan(d_cu, p.B, p.heads, max_tiles, 0, v, s)) != UB_OK) return st;
   const void* mask = p.dropout_mask;
   const int64_t rows = p.T * p.heads;
-  launch_pdl(bwd::bwd_pre_kernel, dim3((unsigned)((rows * 8 + 256 * bwd::kPreRows - 1) / (256 * bwd::kPreRows))), dim3(256), 0, s,
+#ifndef UB_PRE_WAVES
+#define UB_PRE_WAVES 1
+#endif
+  // Delta's grid: UB_PRE_WAVES full waves of resident CTAs (grid-stride), 0 = one CTA per 256 x kPreRows rows
+  static const int pre_per_sm = [] {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, bwd::bwd_pre_kernel, 256, 0);
+    return nb > 0 ? nb : 1;
+  }();
+  const int64_t pre_need = (rows * 8 + 256 * bwd::kPreRows - 1) / (256 * bwd::kPreRows);
+  const int64_t pre_grid =
+      UB_PRE_WAVES > 0 ? std::min<int64_t>(pre_need, (int64_t)sms * pre_per_sm * UB_PRE_WAVES) : pre_need;
+  launch_pdl(bwd::bwd_pre_kernel, dim3((unsigned)pre_grid), dim3(256), 0, s,
              static_cast<const __nv_bfloat16*>(out), static_cast<const __nv_bfloat16*>(dout), delta, p.T, p.heads);
   UB_CHECK_LAUNCH();
 
